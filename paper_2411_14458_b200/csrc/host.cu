@@ -1,0 +1,539 @@
+// host.cu — host side of the batch C ABI (include/geopipe_batch.h).
+//
+// Validates and flattens plan spaces into HBM tables, buckets rows by
+// (policy, stages-per-lane) so each kernel instantiation sees uniform
+// register shapes, launches the evaluation/selection kernels on the
+// context's stream and times them with CUDA events. Host-only arithmetic is
+// limited to what the reference itself evaluates once per scenario with
+// libm (single_tcp_bandwidth, comm_model.cpp:8-25) or exact basic operations
+// (from_ratio, workload.cpp:21-33); every per-row quantity is computed on the
+// device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/geopipe_batch.h"
+#include "device_common.cuh"
+#include "host_internal.h"
+#include "kernels.h"
+
+using namespace gpb;
+
+namespace {
+
+const double kTcpLat[4] = {10.0, 20.0, 30.0, 40.0};
+const double kTcpMbps[4] = {1220.0, 600.0, 396.0, 293.0};  // topology.cpp:45-52
+
+struct ConfigErr {
+  std::string msg;
+};
+
+}  // namespace
+
+// single_tcp_bandwidth (comm_model.cpp:8-25), host libm.
+extern "C" double gpb_single_tcp_bandwidth(const gpb_topology* t, double latency_ms) {
+  double lat[GPB_MAX_TCP], bw[GPB_MAX_TCP];
+  int n;
+  if (t->n_tcp > 0) {
+    n = t->n_tcp;
+    for (int i = 0; i < n; ++i) {
+      lat[i] = t->tcp_latency_ms[i];
+      bw[i] = t->tcp_bw[i];
+    }
+  } else {
+    n = 4;
+    for (int i = 0; i < 4; ++i) {
+      lat[i] = kTcpLat[i];
+      bw[i] = kTcpMbps[i] * 125.0;  // mbps_to_bytes_per_ms (base.h:24)
+    }
+  }
+  if (latency_ms <= lat[0]) return bw[0];
+  if (latency_ms >= lat[n - 1]) return bw[n - 1] * lat[n - 1] / latency_ms;
+  for (int i = 1; i < n; ++i) {
+    if (latency_ms > lat[i]) continue;
+    if (latency_ms == lat[i]) return bw[i];
+    double f = (std::log(latency_ms) - std::log(lat[i - 1])) /
+               (std::log(lat[i]) - std::log(lat[i - 1]));
+    return std::exp(std::log(bw[i - 1]) + f * (std::log(bw[i]) - std::log(bw[i - 1])));
+  }
+  return bw[n - 1];
+}
+
+extern "C" double gpb_repeated_sum_host(double u, long long G) { return repeated_sum(u, G); }
+
+namespace gpb {
+
+void Ctx::set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  last_error = buf;
+}
+
+int Ctx::cuda_fail(cudaError_t e, const char* what) {
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return GPB_ERROR;
+}
+
+void* Ctx::dev_buf(Buf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.bytes < bytes) {
+    if (b.ptr) cudaFree(b.ptr);
+    b.ptr = nullptr;
+    b.bytes = 0;
+    if (cudaMalloc(&b.ptr, bytes) != cudaSuccess) return nullptr;
+    b.bytes = bytes;
+  }
+  return b.ptr;
+}
+
+Ctx::~Ctx() {
+  for (Buf* b : all_bufs()) {
+    if (b->ptr) cudaFree(b->ptr);
+  }
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (ev2) cudaEventDestroy(ev2);
+  if (ev3) cudaEventDestroy(ev3);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+// ------------------------------------------------------------ validation
+
+static void validate_topology(const gpb_topology& t, int idx) {
+  char p[64];
+  snprintf(p, sizeof p, "topologies[%d]", idx);
+  if (t.n_dc < 1 || t.n_dc > GPB_MAX_DC)
+    throw ConfigErr{std::string(p) + ".n_dc: must be in [1, 8]"};
+  for (int i = 0; i < t.n_dc; ++i) {
+    if (t.gpu_count[i] < 0) throw ConfigErr{std::string(p) + ".gpu_count: must be >= 0"};
+    if (!(t.intra_bw[i] > 0)) throw ConfigErr{std::string(p) + ".intra_bw: must be > 0"};
+    for (int j = 0; j < t.n_dc; ++j)
+      if (!(t.latency_ms[i][j] >= 0))
+        throw ConfigErr{std::string(p) + ".latency_ms: must be >= 0"};
+  }
+  if (!(t.pair_bw_cap > 0)) throw ConfigErr{std::string(p) + ".pair_bw_cap: must be > 0"};
+  if (t.n_tcp < 0 || t.n_tcp > GPB_MAX_TCP)
+    throw ConfigErr{std::string(p) + ".n_tcp: must be in [0, 8]"};
+  for (int i = 0; i < t.n_tcp; ++i) {  // validate_tcp_table (topology.cpp:56-76)
+    if (t.tcp_latency_ms[i] <= 0 || t.tcp_bw[i] <= 0)
+      throw ConfigErr{"wan.tcp_table: latency and bandwidth must be positive"};
+    if (i > 0 && t.tcp_latency_ms[i] <= t.tcp_latency_ms[i - 1])
+      throw ConfigErr{"wan.tcp_table: latencies must be strictly increasing"};
+    if (i > 0 && t.tcp_bw[i] >= t.tcp_bw[i - 1])
+      throw ConfigErr{"wan.tcp_table: bandwidths must be strictly decreasing"};
+  }
+}
+
+static int64_t act_bytes(const gpb_scenario& s) {
+  return s.microbatch * s.seq_len * s.hidden * (int64_t)s.bytes_per_element;
+}
+
+static void validate_scenario(const gpb_scenario& s, int idx, int n_topo,
+                              const gpb_topology* topos) {
+  char p[64];
+  snprintf(p, sizeof p, "scenarios[%d]", idx);
+  const std::string P(p);
+  if (s.topology < 0 || s.topology >= n_topo) throw ConfigErr{P + ".topology: out of range"};
+  const gpb_topology& t = topos[s.topology];
+  if (s.policy < 0 || s.policy > 3)
+    throw ConfigErr{"policy: must be one of gpipe, 1f1b, varuna, atlas"};
+  if (s.pipelines_per_cell < 1) throw ConfigErr{"select.pipelines_per_cell: must be >= 1"};
+  if (s.tp_degree < 1) throw ConfigErr{"select.tp_degree: must be >= 1"};
+  if (s.num_layers < 1) throw ConfigErr{"model.num_layers: must be >= 1"};
+  if (s.layers_per_partition < 1) throw ConfigErr{"model.layers_per_partition: must be >= 1"};
+  if (s.num_microbatches < 1) throw ConfigErr{"model.num_microbatches: must be >= 1"};
+  if (s.bytes_per_element < 1 || s.hidden < 1 || s.seq_len < 1 || s.microbatch < 1)
+    throw ConfigErr{"model: dimensions must be >= 1"};
+  if (s.params_per_layer < 0) throw ConfigErr{"model.params_per_layer: must be >= 0"};
+  if (s.ratio_C > 0) {
+  } else if (s.ratio_C < 0) {
+    throw ConfigErr{"compute.ratio_C: must be > 0"};
+  } else if (!(s.fwd_ms > 0) || !(s.bwd_ms > 0) || s.recompute_ms < 0) {
+    throw ConfigErr{"compute: durations must be positive"};  // workload.cpp:11-13
+  }
+  if (s.d_max < 0) throw ConfigErr{"select.d_max: must be >= 1"};
+  if (s.n_order < 0 || s.n_order > t.n_dc) throw ConfigErr{P + ".n_order: out of range"};
+  unsigned seen = 0;
+  for (int i = 0; i < s.n_order; ++i) {
+    const int dc = s.dc_order[i];
+    if (dc < 0 || dc >= t.n_dc) throw ConfigErr{"datacenters: unknown datacenter id"};
+    if (seen & (1u << dc))
+      throw ConfigErr{P + ".dc_order: duplicate datacenter (unsupported, see DESIGN.md)"};
+    seen |= 1u << dc;
+  }
+  if (s.mem_limit < 0) throw ConfigErr{"mem_limit: must be >= 1"};
+  if (s.multi_conn && s.n_connections < 1)
+    throw ConfigErr{"simulate.n_connections: must be >= 1"};
+  const int S = (s.num_layers + s.layers_per_partition - 1) / s.layers_per_partition;
+  if (S > 256)
+    throw ConfigErr{P + ": more than 256 pipeline stages is outside the kernel envelope"};
+  if (s.policy == GPB_ATLAS && (long long)s.pipelines_per_cell * S > 4096)
+    throw ConfigErr{P + ": atlas with C*S > 4096 is outside the kernel envelope"};
+  if (act_bytes(s) <= 0) throw ConfigErr{"model: activation size overflow"};
+}
+
+}  // namespace gpb
+
+// --------------------------------------------------------------- API
+
+extern "C" {
+
+gpb_ctx* gpb_create(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return nullptr;
+  Ctx* c = new Ctx();
+  c->device = device;
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  c->num_sms = prop.multiProcessorCount;
+  c->smem_optin = (int)prop.sharedMemPerBlockOptin;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
+      cudaEventCreate(&c->ev2) != cudaSuccess || cudaEventCreate(&c->ev3) != cudaSuccess) {
+    delete c;
+    return nullptr;
+  }
+  return reinterpret_cast<gpb_ctx*>(c);
+}
+
+void gpb_destroy(gpb_ctx* ctx) { delete reinterpret_cast<Ctx*>(ctx); }
+
+const char* gpb_last_error(gpb_ctx* ctx) {
+  return ctx ? reinterpret_cast<Ctx*>(ctx)->last_error.c_str() : "";
+}
+
+int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
+             const gpb_scenario* scens, int32_t n_scen, int64_t* n_rows_out) {
+  if (!ctx_) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  c.last_error.clear();
+  c.loaded = false;
+  if (cudaSetDevice(c.device) != cudaSuccess) return c.cuda_fail(cudaGetLastError(), "set device");
+  if (n_scen < 0 || n_topo < 0 || (n_scen > 0 && (!topos || !scens))) {
+    c.set_error("null input");
+    return GPB_CONFIG_ERROR;
+  }
+  std::vector<DevTopo> dt(std::max(n_topo, 1));
+  std::vector<DevScen> ds(std::max(n_scen, 1));
+  std::vector<int32_t> row_scen;
+  try {
+    for (int i = 0; i < n_topo; ++i) {
+      validate_topology(topos[i], i);
+      const gpb_topology& t = topos[i];
+      DevTopo& d = dt[i];
+      std::memset(&d, 0, sizeof d);
+      d.n_dc = t.n_dc;
+      int base = 0;
+      for (int a = 0; a < t.n_dc; ++a) {
+        d.gpu_count[a] = t.gpu_count[a];
+        d.dc_base[a] = base;
+        base += t.gpu_count[a];
+        d.intra_bw[a] = t.intra_bw[a];
+        for (int b = 0; b < t.n_dc; ++b) {
+          // latency_between (topology.cpp:21-30): symmetric by unordered pair
+          const double lat = a == b ? 0.0 : t.latency_ms[std::min(a, b)][std::max(a, b)];
+          d.lat_ms[a][b] = lat;
+          d.single_bw[a][b] = gpb_single_tcp_bandwidth(&t, lat);
+        }
+      }
+      d.pair_cap = t.pair_bw_cap;
+    }
+    int64_t row = 0;
+    for (int i = 0; i < n_scen; ++i) {
+      validate_scenario(scens[i], i, n_topo, topos);
+      const gpb_scenario& s = scens[i];
+      const gpb_topology& t = topos[s.topology];
+      DevScen& d = ds[i];
+      std::memset(&d, 0, sizeof d);
+      d.topo = s.topology;
+      d.policy = s.policy;
+      d.S = (s.num_layers + s.layers_per_partition - 1) / s.layers_per_partition;
+      d.M = s.num_microbatches;
+      d.C = s.pipelines_per_cell;
+      d.tp = s.tp_degree;
+      d.L = s.num_layers;
+      d.lpp = s.layers_per_partition;
+      d.recompute = s.recompute ? 1 : 0;
+      d.mem_limit = s.mem_limit > 0 ? s.mem_limit : d.S;  // scheduler.cpp:561
+      d.n_conns = s.multi_conn ? s.n_connections : 1;
+      d.bytes = act_bytes(s);
+      d.ppl = s.params_per_layer > 0 ? s.params_per_layer
+                                     : 12.0 * (double)s.hidden * (double)s.hidden;
+      if (s.ratio_C > 0) {  // from_ratio (workload.cpp:21-33)
+        const double comm_ms = (double)d.bytes / t.pair_bw_cap;
+        d.fwd_ms = comm_ms / s.ratio_C;
+        d.bwd_ms = 2.0 * d.fwd_ms;
+        d.rec_ms = d.fwd_ms;
+      } else {
+        d.fwd_ms = s.fwd_ms;
+        d.bwd_ms = s.bwd_ms;
+        d.rec_ms = s.recompute_ms;
+      }
+      int order[GPB_MAX_DC];
+      int n_order = s.n_order;
+      if (n_order > 0) {
+        for (int k = 0; k < n_order; ++k) order[k] = s.dc_order[k];
+      } else {  // default_dc_order (workload.cpp:47-55): stable, count desc
+        n_order = t.n_dc;
+        for (int k = 0; k < n_order; ++k) order[k] = k;
+        std::stable_sort(order, order + n_order,
+                         [&](int a, int b) { return t.gpu_count[a] > t.gpu_count[b]; });
+      }
+      d.n_order = n_order;
+      for (int k = 0; k < n_order; ++k) d.order[k] = (int8_t)order[k];
+      long long total = 0;
+      for (int k = 0; k < t.n_dc; ++k) total += t.gpu_count[k];
+      const long long per_cell = (long long)d.C * d.S * d.tp;
+      const int dflt = (int)std::max<long long>(0, total / per_cell);  // dc_select.cpp:20-25
+      const int d_max = std::max(1, s.d_max > 0 ? s.d_max : dflt);
+      d.first_row = row;
+      d.n_rows = d_max;
+      row += d_max;
+      if (row > (int64_t)1 << 31) throw ConfigErr{"plan space exceeds 2^31 rows"};
+    }
+    row_scen.resize(row);
+    for (int i = 0; i < n_scen; ++i)
+      for (int k = 0; k < ds[i].n_rows; ++k) row_scen[ds[i].first_row + k] = i;
+  } catch (const ConfigErr& e) {
+    c.last_error = e.msg;
+    return GPB_CONFIG_ERROR;
+  }
+  const int64_t n_rows = (int64_t)row_scen.size();
+
+  // Buckets: (policy, B = ceil(S/32)); within a bucket scenarios are dealt
+  // in decreasing estimated cost so the persistent warps finish together.
+  c.buckets.clear();
+  std::map<std::pair<int, int>, std::vector<int>> by_key;
+  for (int i = 0; i < n_scen; ++i) by_key[{ds[i].policy, (ds[i].S + 31) / 32}].push_back(i);
+  std::vector<int32_t> work;
+  work.reserve(n_rows);
+  for (auto& [key, list] : by_key) {
+    auto cost = [&](int i) {
+      const DevScen& d = ds[i];
+      double base = (double)d.M * d.S;
+      return d.policy == GPB_ATLAS ? base * d.C * d.C : base;
+    };
+    std::stable_sort(list.begin(), list.end(), [&](int a, int b) { return cost(a) > cost(b); });
+    Bucket b;
+    b.policy = key.first;
+    b.B = key.second;
+    b.offset = (int32_t)work.size();
+    for (int i : list) {
+      for (int k = 0; k < ds[i].n_rows; ++k) work.push_back((int32_t)(ds[i].first_row + k));
+      b.max_m = std::max(b.max_m, ds[i].M);
+      b.max_cs = std::max(b.max_cs, ds[i].C * ds[i].S);
+      b.max_cm = std::max(b.max_cm, ds[i].C * ds[i].M);
+      b.max_csm = std::max(b.max_csm, (long long)ds[i].C * ds[i].S * ds[i].M);
+    }
+    b.count = (int32_t)work.size() - b.offset;
+    c.buckets.push_back(b);
+  }
+
+  // Upload (one H2D per table).
+  cudaStream_t st = c.stream;
+  auto up = [&](Buf& b, const void* src, size_t bytes) -> bool {
+    void* p = c.dev_buf(b, bytes);
+    if (!p) return false;
+    return bytes == 0 || cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, st) == cudaSuccess;
+  };
+  if (!up(c.b_topos, dt.data(), sizeof(DevTopo) * dt.size()) ||
+      !up(c.b_scens, ds.data(), sizeof(DevScen) * ds.size()) ||
+      !up(c.b_row_scen, row_scen.data(), sizeof(int32_t) * row_scen.size()) ||
+      !up(c.b_work, work.data(), sizeof(int32_t) * work.size()) ||
+      !c.dev_buf(c.b_rows, sizeof(gpb_row) * std::max<int64_t>(n_rows, 1)) ||
+      !c.dev_buf(c.b_results, sizeof(gpb_scenario_result) * std::max(n_scen, 1)) ||
+      !c.dev_buf(c.b_cursors, sizeof(int32_t) * (c.buckets.size() + 1)) ||
+      !c.dev_buf(c.b_best, sizeof(gpb_best) * 1024)) {
+    return c.cuda_fail(cudaGetLastError(), "upload");
+  }
+  c.h2d_bytes = sizeof(DevTopo) * dt.size() + sizeof(DevScen) * ds.size() +
+                sizeof(int32_t) * (row_scen.size() + work.size());
+  c.n_rows = n_rows;
+  c.n_scen = n_scen;
+  c.n_topo = n_topo;
+  c.host_scens.assign(scens, scens + n_scen);
+  c.host_topos.assign(topos, topos + n_topo);
+  c.dev_scens_host = ds;
+  c.dev_topos_host = dt;
+  c.row_scen_host = row_scen;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return c.cuda_fail(cudaGetLastError(), "upload");
+  c.loaded = true;
+  if (n_rows_out) *n_rows_out = n_rows;
+  return GPB_OK;
+}
+
+int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
+  if (!ctx_) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  c.last_error.clear();
+  if (!c.loaded) {
+    c.set_error("no plan space loaded");
+    return GPB_CONFIG_ERROR;
+  }
+  cudaSetDevice(c.device);
+  cudaStream_t st = c.stream;
+  int32_t* cursors = (int32_t*)c.b_cursors.ptr;
+  int32_t* err_flag = cursors + c.buckets.size();
+  cudaEventRecord(c.ev0, st);
+  cudaMemsetAsync(cursors, 0, sizeof(int32_t) * (c.buckets.size() + 1), st);
+  int launches = 0;
+  const int grid_eval = c.num_sms * 8;
+  for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
+    const Bucket& b = c.buckets[bi];
+    if (b.count == 0) continue;
+    EvalArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.scens = (const DevScen*)c.b_scens.ptr;
+    a.topos = (const DevTopo*)c.b_topos.ptr;
+    a.row_scen = (const int32_t*)c.b_row_scen.ptr;
+    a.work = (const int32_t*)c.b_work.ptr + b.offset;
+    a.n_work = b.count;
+    a.cursor = cursors + bi;
+    a.rows = (gpb_row*)c.b_rows.ptr;
+    a.error_flag = err_flag;
+    const int grid = std::min(grid_eval, (b.count + 3) / 4);
+    cudaError_t e;
+    if (b.policy == GPB_GPIPE || b.policy == GPB_VARUNA) {
+      a.smem_m = b.max_m;
+      const size_t smem = (size_t)(kEvalThreads / 32) * b.max_m * 8;
+      if ((int)smem > c.smem_optin) {
+        c.set_error("num_microbatches too large for the flush kernel's shared buffer");
+        return GPB_CONFIG_ERROR;
+      }
+      e = launch_flush(b.B, b.policy == GPB_GPIPE, a, grid, st);
+    } else if (b.policy == GPB_1F1B) {
+      e = launch_onef1b(b.B, a, grid, st);
+    } else {
+      a.smem_cs = b.max_cs;
+      a.smem_warp_bytes = (int32_t)(((size_t)16 * 8 + (size_t)b.max_cs * 20 + 15) / 16 * 16);
+      if ((size_t)a.smem_warp_bytes * (kEvalThreads / 32) > (size_t)c.smem_optin) {
+        c.set_error("atlas C*S too large for the shared slice");
+        return GPB_CONFIG_ERROR;
+      }
+      a.res_cap = b.max_cm;
+      a.scratch_csm = b.max_csm;
+      a.scratch_cm = b.max_cm;
+      a.scratch_per_warp = b.max_csm + b.max_cm + 2LL * (GPB_MAX_DC - 1) * b.max_cm;
+      const int agrid = std::min(grid, c.num_sms * 8);
+      void* scr = c.dev_buf(c.b_scratch, sizeof(long long) * a.scratch_per_warp *
+                                             (size_t)agrid * (kEvalThreads / 32));
+      if (!scr) return c.cuda_fail(cudaErrorMemoryAllocation, "atlas scratch");
+      a.scratch = (long long*)scr;
+      e = launch_atlas(a, agrid, st);
+    }
+    if (e != cudaSuccess) return c.cuda_fail(e, "eval launch");
+    ++launches;
+  }
+  cudaEventRecord(c.ev1, st);
+  SelectArgs sa;
+  sa.scens = (const DevScen*)c.b_scens.ptr;
+  sa.n_scen = c.n_scen;
+  sa.rows = (gpb_row*)c.b_rows.ptr;
+  sa.results = (gpb_scenario_result*)c.b_results.ptr;
+  sa.block_best = (gpb_best*)c.b_best.ptr + 1;
+  sa.best = (gpb_best*)c.b_best.ptr;
+  const int sgrid = std::max(1, std::min(1023, (c.n_scen + 3) / 4));
+  cudaError_t e = launch_select(sa, sgrid, st);
+  if (e != cudaSuccess) return c.cuda_fail(e, "select launch");
+  launches += 2;
+  cudaEventRecord(c.ev2, st);
+  c.last_launches = launches + 1;  // + the cursor memset
+  c.timing_valid = true;
+  if (sync) {
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return c.cuda_fail(e, "evaluate");
+    return c.check_error_flag();
+  }
+  return GPB_OK;
+}
+
+int gpb_fetch_rows(gpb_ctx* ctx_, gpb_row* rows, int64_t n) {
+  if (!ctx_) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  if (!c.loaded) {
+    c.set_error("no plan space loaded");
+    return GPB_CONFIG_ERROR;
+  }
+  cudaSetDevice(c.device);
+  if (rows && n > 0) {
+    n = std::min(n, c.n_rows);
+    cudaError_t e = cudaMemcpyAsync(rows, c.b_rows.ptr, sizeof(gpb_row) * n,
+                                    cudaMemcpyDeviceToHost, c.stream);
+    if (e != cudaSuccess) return c.cuda_fail(e, "fetch rows");
+  }
+  cudaError_t e = cudaStreamSynchronize(c.stream);
+  if (e != cudaSuccess) return c.cuda_fail(e, "fetch rows");
+  return c.check_error_flag();
+}
+
+int gpb_fetch_scenarios(gpb_ctx* ctx_, gpb_scenario_result* out, int32_t n) {
+  if (!ctx_) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  cudaSetDevice(c.device);
+  if (out && n > 0) {
+    n = std::min(n, c.n_scen);
+    cudaError_t e = cudaMemcpyAsync(out, c.b_results.ptr, sizeof(gpb_scenario_result) * n,
+                                    cudaMemcpyDeviceToHost, c.stream);
+    if (e != cudaSuccess) return c.cuda_fail(e, "fetch scenarios");
+  }
+  cudaError_t e = cudaStreamSynchronize(c.stream);
+  if (e != cudaSuccess) return c.cuda_fail(e, "fetch scenarios");
+  return c.check_error_flag();
+}
+
+int gpb_fetch_best(gpb_ctx* ctx_, gpb_best* out) {
+  if (!ctx_) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  cudaSetDevice(c.device);
+  cudaError_t e = cudaMemcpyAsync(out, c.b_best.ptr, sizeof(gpb_best), cudaMemcpyDeviceToHost,
+                                  c.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+  if (e != cudaSuccess) return c.cuda_fail(e, "fetch best");
+  return c.check_error_flag();
+}
+
+void* gpb_device_best(gpb_ctx* ctx_) {
+  if (!ctx_) return nullptr;
+  return reinterpret_cast<Ctx*>(ctx_)->b_best.ptr;
+}
+
+int gpb_get_timing(gpb_ctx* ctx_, gpb_timing* out) {
+  if (!ctx_ || !out) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  std::memset(out, 0, sizeof *out);
+  if (c.timing_valid) {
+    cudaEventSynchronize(c.ev2);
+    cudaEventElapsedTime(&out->evaluate_ms, c.ev0, c.ev2);
+    cudaEventElapsedTime(&out->timing_kernels_ms, c.ev0, c.ev1);
+    cudaEventElapsedTime(&out->select_ms, c.ev1, c.ev2);
+  }
+  out->pack_ms = c.pack_ms;
+  out->launches = c.last_launches;
+  return GPB_OK;
+}
+
+}  // extern "C"
+
+namespace gpb {
+int Ctx::check_error_flag() {
+  int32_t flag = 0;
+  int32_t* cursors = (int32_t*)b_cursors.ptr;
+  if (!cursors) return GPB_OK;
+  cudaMemcpy(&flag, cursors + buckets.size(), sizeof flag, cudaMemcpyDeviceToHost);
+  if (flag) {
+    set_error("kernel invariant failure (see rows with feasible == -1)");
+    return GPB_ERROR;
+  }
+  return GPB_OK;
+}
+}  // namespace gpb

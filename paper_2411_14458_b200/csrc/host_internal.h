@@ -1,0 +1,74 @@
+// host_internal.h — the batch context behind the opaque gpb_ctx handle.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/geopipe_batch.h"
+#include "device_common.cuh"
+
+namespace gpb {
+
+struct Buf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct Bucket {
+  int policy = 0;
+  int B = 1;            // stages per lane = ceil(S / 32)
+  int32_t offset = 0;   // into the work list
+  int32_t count = 0;
+  int max_m = 0;
+  int max_cs = 0;
+  int max_cm = 0;
+  long long max_csm = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  int smem_optin = 227 * 1024;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  std::string last_error;
+
+  bool loaded = false;
+  int64_t n_rows = 0;
+  int32_t n_scen = 0, n_topo = 0;
+  size_t h2d_bytes = 0;
+  std::vector<Bucket> buckets;
+  std::vector<gpb_scenario> host_scens;
+  std::vector<gpb_topology> host_topos;
+  std::vector<DevScen> dev_scens_host;
+  std::vector<DevTopo> dev_topos_host;
+  std::vector<int32_t> row_scen_host;
+
+  // device tables
+  Buf b_topos, b_scens, b_row_scen, b_work, b_rows, b_results, b_cursors, b_best;
+  Buf b_scratch;
+  // timeline / bubbletea buffers
+  Buf b_tl_rows, b_tl_spans, b_tl_nspan, b_tl_scratch, b_gaps, b_ngaps, b_reqs, b_pl,
+      b_sum, b_pack_scratch, b_pack_misc;
+
+  bool timing_valid = false;
+  int last_launches = 0;
+  float pack_ms = 0.f;
+
+  std::vector<Buf*> all_bufs() {
+    return {&b_topos, &b_scens, &b_row_scen, &b_work, &b_rows, &b_results, &b_cursors,
+            &b_best, &b_scratch, &b_tl_rows, &b_tl_spans, &b_tl_nspan, &b_tl_scratch,
+            &b_gaps, &b_ngaps, &b_reqs, &b_pl, &b_sum, &b_pack_scratch, &b_pack_misc};
+  }
+
+  void set_error(const char* fmt, ...);
+  int cuda_fail(cudaError_t e, const char* what);
+  void* dev_buf(Buf& b, size_t bytes);
+  int check_error_flag();
+  ~Ctx();
+};
+
+}  // namespace gpb

@@ -1,0 +1,53 @@
+// kernels.h — launch interface between the host planner (host.cpp) and the
+// sm_100a kernels. Plain structs of device pointers; no torch types.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/geopipe_batch.h"
+
+namespace gpb {
+
+struct DevTopo;
+struct DevScen;
+
+constexpr int kEvalThreads = 128;  // 4 warps per CTA, one plan row per warp
+
+struct EvalArgs {
+  const DevScen* scens;
+  const DevTopo* topos;
+  const int32_t* row_scen;    // row -> scenario
+  const int32_t* work;        // rows of this bucket, in dispatch order
+  int32_t n_work;
+  int32_t* cursor;            // atomic work cursor (zeroed per launch)
+  gpb_row* rows;              // output table
+  int32_t* error_flag;
+  // flush: per-warp shared fd_last buffer length (max M of the bucket)
+  int32_t smem_m;
+  // atlas: per-warp shared slice and global scratch layout
+  int32_t smem_cs;            // max C*S of the bucket
+  int32_t smem_warp_bytes;
+  int32_t res_cap;            // max C*M of the bucket
+  long long* scratch;
+  long long scratch_per_warp; // int64 elements
+  long long scratch_csm;      // max C*S*M
+  long long scratch_cm;       // max C*M
+};
+
+struct SelectArgs {
+  const DevScen* scens;
+  int32_t n_scen;
+  gpb_row* rows;
+  gpb_scenario_result* results;
+  gpb_best* block_best;       // [grid]
+  gpb_best* best;
+};
+
+cudaError_t launch_flush(int B, bool gpipe, const EvalArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_onef1b(int B, const EvalArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_atlas(const EvalArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_select(const SelectArgs& a, int grid, cudaStream_t st);
+
+}  // namespace gpb
