@@ -201,9 +201,18 @@ int gpb_fetch_rows(gpb_ctx* ctx, gpb_row* rows, int64_t n_rows);
 int gpb_fetch_scenarios(gpb_ctx* ctx, gpb_scenario_result* out, int32_t n_scen);
 int gpb_fetch_best(gpb_ctx* ctx, gpb_best* out);
 
+/* Launch on an external stream (e.g. the caller's framework stream);
+ * NULL restores the context's own stream. */
+int gpb_set_stream(gpb_ctx* ctx, void* cuda_stream);
+
 /* Device address of the batch's gpb_best record (for an NCCL all-gather of
  * per-GPU winners). */
 void* gpb_device_best(gpb_ctx* ctx);
+
+/* Asynchronous device-to-device copy of the gpb_best record (16 bytes) to
+ * `dst` on the launch stream (feeds an NCCL all-gather without a host
+ * round trip). */
+int gpb_copy_best(gpb_ctx* ctx, void* dst);
 
 /* Bubbles of one row's iteration timeline (run(), engine.cpp:452-460) over
  * [0, horizon_ns) (horizon_ns <= 0 => makespan), sorted (gpu, start) like
@@ -232,10 +241,18 @@ typedef struct gpb_timing {
   float timing_kernels_ms;     /* schedule-timing kernels only */
   float select_ms;             /* selection kernels */
   float pack_ms;               /* last gpb_pack_prefills */
+  float policy_ms[4];          /* timing kernels per policy (GPB_GPIPE..) */
   int32_t launches;            /* kernels launched by the last call */
   int32_t pad_;
+  int64_t h2d_bytes;           /* bytes uploaded by the last gpb_load */
+  int64_t d2h_bytes;           /* bytes fetched since the last gpb_load */
 } gpb_timing;
 int gpb_get_timing(gpb_ctx* ctx, gpb_timing* out);
+
+/* On-device issue-rate microbenchmark used as the roofline denominator:
+ * kind 0 = int64 max-plus ops (one max or one add = 1 op) in independent
+ * register chains over every SM. Returns Gop/s. */
+int gpb_microbench(gpb_ctx* ctx, int32_t kind, double* gops);
 
 #ifdef __cplusplus
 } /* extern "C" */

@@ -170,8 +170,11 @@ class Timing(C.Structure):
         ("timing_kernels_ms", C.c_float),
         ("select_ms", C.c_float),
         ("pack_ms", C.c_float),
+        ("policy_ms", C.c_float * 4),
         ("launches", C.c_int32),
         ("pad_", C.c_int32),
+        ("h2d_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64),
     ]
 
 

@@ -104,7 +104,8 @@ Ctx::~Ctx() {
   if (ev1) cudaEventDestroy(ev1);
   if (ev2) cudaEventDestroy(ev2);
   if (ev3) cudaEventDestroy(ev3);
-  if (stream) cudaStreamDestroy(stream);
+  for (cudaEvent_t e : bucket_ev) cudaEventDestroy(e);
+  if (own_stream) cudaStreamDestroy(own_stream);
 }
 
 // ------------------------------------------------------------ validation
@@ -198,12 +199,13 @@ gpb_ctx* gpb_create(int device) {
   cudaGetDeviceProperties(&prop, device);
   c->num_sms = prop.multiProcessorCount;
   c->smem_optin = (int)prop.sharedMemPerBlockOptin;
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+  if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaEventCreate(&c->ev2) != cudaSuccess || cudaEventCreate(&c->ev3) != cudaSuccess) {
     delete c;
     return nullptr;
   }
+  c->stream = c->own_stream;
   return reinterpret_cast<gpb_ctx*>(c);
 }
 
@@ -357,6 +359,7 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
       !c.dev_buf(c.b_best, sizeof(gpb_best) * 1024)) {
     return c.cuda_fail(cudaGetLastError(), "upload");
   }
+  c.d2h_bytes = 0;
   c.h2d_bytes = sizeof(DevTopo) * dt.size() + sizeof(DevScen) * ds.size() +
                 sizeof(int32_t) * (row_scen.size() + work.size());
   c.n_rows = n_rows;
@@ -389,8 +392,14 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
   cudaMemsetAsync(cursors, 0, sizeof(int32_t) * (c.buckets.size() + 1), st);
   int launches = 0;
   const int grid_eval = c.num_sms * 8;
+  while (c.bucket_ev.size() < c.buckets.size() + 1) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return c.cuda_fail(cudaGetLastError(), "event");
+    c.bucket_ev.push_back(e);
+  }
   for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
     const Bucket& b = c.buckets[bi];
+    cudaEventRecord(c.bucket_ev[bi], st);
     if (b.count == 0) continue;
     EvalArgs a;
     std::memset(&a, 0, sizeof a);
@@ -435,6 +444,7 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     if (e != cudaSuccess) return c.cuda_fail(e, "eval launch");
     ++launches;
   }
+  cudaEventRecord(c.bucket_ev[c.buckets.size()], st);
   cudaEventRecord(c.ev1, st);
   SelectArgs sa;
   sa.scens = (const DevScen*)c.b_scens.ptr;
@@ -469,6 +479,7 @@ int gpb_fetch_rows(gpb_ctx* ctx_, gpb_row* rows, int64_t n) {
     n = std::min(n, c.n_rows);
     cudaError_t e = cudaMemcpyAsync(rows, c.b_rows.ptr, sizeof(gpb_row) * n,
                                     cudaMemcpyDeviceToHost, c.stream);
+    c.d2h_bytes += (int64_t)sizeof(gpb_row) * n;
     if (e != cudaSuccess) return c.cuda_fail(e, "fetch rows");
   }
   cudaError_t e = cudaStreamSynchronize(c.stream);
@@ -502,6 +513,21 @@ int gpb_fetch_best(gpb_ctx* ctx_, gpb_best* out) {
   return c.check_error_flag();
 }
 
+int gpb_copy_best(gpb_ctx* ctx_, void* dst) {
+  if (!ctx_ || !dst) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  cudaError_t e = cudaMemcpyAsync(dst, c.b_best.ptr, sizeof(gpb_best), cudaMemcpyDeviceToDevice,
+                                  c.stream);
+  return e == cudaSuccess ? GPB_OK : c.cuda_fail(e, "copy best");
+}
+
+int gpb_set_stream(gpb_ctx* ctx_, void* s) {
+  if (!ctx_) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  c.stream = s ? (cudaStream_t)s : c.own_stream;
+  return GPB_OK;
+}
+
 void* gpb_device_best(gpb_ctx* ctx_) {
   if (!ctx_) return nullptr;
   return reinterpret_cast<Ctx*>(ctx_)->b_best.ptr;
@@ -516,9 +542,16 @@ int gpb_get_timing(gpb_ctx* ctx_, gpb_timing* out) {
     cudaEventElapsedTime(&out->evaluate_ms, c.ev0, c.ev2);
     cudaEventElapsedTime(&out->timing_kernels_ms, c.ev0, c.ev1);
     cudaEventElapsedTime(&out->select_ms, c.ev1, c.ev2);
+    for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c.bucket_ev[bi], c.bucket_ev[bi + 1]);
+      out->policy_ms[c.buckets[bi].policy] += ms;
+    }
   }
   out->pack_ms = c.pack_ms;
   out->launches = c.last_launches;
+  out->h2d_bytes = (int64_t)c.h2d_bytes;
+  out->d2h_bytes = c.d2h_bytes;
   return GPB_OK;
 }
 
@@ -529,7 +562,8 @@ int Ctx::check_error_flag() {
   int32_t flag = 0;
   int32_t* cursors = (int32_t*)b_cursors.ptr;
   if (!cursors) return GPB_OK;
-  cudaMemcpy(&flag, cursors + buckets.size(), sizeof flag, cudaMemcpyDeviceToHost);
+  cudaMemcpyAsync(&flag, cursors + buckets.size(), sizeof flag, cudaMemcpyDeviceToHost, stream);
+  cudaStreamSynchronize(stream);
   if (flag) {
     set_error("kernel invariant failure (see rows with feasible == -1)");
     return GPB_ERROR;
@@ -537,3 +571,30 @@ int Ctx::check_error_flag() {
   return GPB_OK;
 }
 }  // namespace gpb
+
+extern "C" int gpb_microbench(gpb_ctx* ctx_, int32_t kind, double* gops) {
+  if (!ctx_ || !gops) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  if (kind != 0) {
+    c.set_error("unknown microbenchmark kind");
+    return GPB_CONFIG_ERROR;
+  }
+  cudaSetDevice(c.device);
+  void* out = c.dev_buf(c.b_pack_misc, 64);
+  const int grid = c.num_sms * 8, iters = 4096;
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(c.ev0, c.stream);
+    cudaError_t e = launch_maxplus_bench((long long*)out, grid, iters, c.stream);
+    if (e != cudaSuccess) return c.cuda_fail(e, "microbench");
+    cudaEventRecord(c.ev3, c.stream);
+    cudaEventSynchronize(c.ev3);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c.ev0, c.ev3);
+    if (rep > 0 && ms < best) best = ms;
+  }
+  const double ops = (double)grid * 256 * iters * 8 * 2;
+  *gops = ops / (best * 1e-3) / 1e9;
+  c.timing_valid = false;
+  return GPB_OK;
+}

@@ -32,7 +32,9 @@ struct Ctx {
   int device = 0;
   int num_sms = 148;
   int smem_optin = 227 * 1024;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;     // active launch stream
+  cudaStream_t own_stream = nullptr; // the context's own stream
+  int64_t d2h_bytes = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
   std::string last_error;
 
@@ -54,6 +56,7 @@ struct Ctx {
   Buf b_tl_rows, b_tl_spans, b_tl_nspan, b_tl_scratch, b_gaps, b_ngaps, b_reqs, b_pl,
       b_sum, b_pack_scratch, b_pack_misc;
 
+  std::vector<cudaEvent_t> bucket_ev;  // [buckets + 1]
   bool timing_valid = false;
   int last_launches = 0;
   float pack_ms = 0.f;

@@ -51,3 +51,7 @@ cudaError_t launch_atlas(const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_select(const SelectArgs& a, int grid, cudaStream_t st);
 
 }  // namespace gpb
+
+namespace gpb {
+cudaError_t launch_maxplus_bench(long long* out, int grid, int iters, cudaStream_t st);
+}

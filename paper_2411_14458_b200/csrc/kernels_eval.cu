@@ -876,3 +876,32 @@ cudaError_t launch_select(const SelectArgs& a, int grid, cudaStream_t st) {
 }
 
 }  // namespace gpb
+
+// ------------------------------------------------------- microbenchmark
+
+namespace gpb {
+
+// Peak int64 max-plus issue rate: 8 independent chains per thread of
+// x = max(x + a, y) (2 ops per update), every SM fully occupied.
+__global__ void __launch_bounds__(256) maxplus_bench_kernel(long long* out, int iters,
+                                                             long long a, long long y0) {
+  long long x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x + k;
+  long long y = y0 + blockIdx.x;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = imax(x[k] + a, y + k);
+  }
+  long long s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s ^= x[k];
+  if (s == 0x5a5a5a5a5a5a5aLL) out[0] = s;
+}
+
+cudaError_t launch_maxplus_bench(long long* out, int grid, int iters, cudaStream_t st) {
+  maxplus_bench_kernel<<<grid, 256, 0, st>>>(out, iters, 3, 1LL << 40);
+  return cudaGetLastError();
+}
+
+}  // namespace gpb

@@ -73,6 +73,9 @@ def load_library(path: str = LIB_PATH):
         "gpb_synthetic_requests": (C.c_int, [C.c_int32, C.c_uint32, C.c_double,
                                              P(abi.PrefillModel), P(abi.Request)]),
         "gpb_get_timing": (C.c_int, [C.c_void_p, P(abi.Timing)]),
+        "gpb_microbench": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_double)]),
+        "gpb_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+        "gpb_copy_best": (C.c_int, [C.c_void_p, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -86,7 +89,8 @@ def exported_symbols():
     return ["gpb_create", "gpb_destroy", "gpb_last_error", "gpb_single_tcp_bandwidth",
             "gpb_load", "gpb_evaluate", "gpb_fetch_rows", "gpb_fetch_scenarios",
             "gpb_fetch_best", "gpb_device_best", "gpb_bubbles", "gpb_pack_prefills",
-            "gpb_synthetic_requests", "gpb_get_timing"]
+            "gpb_synthetic_requests", "gpb_get_timing", "gpb_microbench", "gpb_set_stream",
+            "gpb_copy_best"]
 
 
 @dataclass
@@ -164,6 +168,13 @@ class Planner:
         self._check(self.lib.gpb_fetch_best(self.ctx, C.byref(b)))
         return b
 
+    def set_stream(self, cuda_stream: int | None):
+        self._check(self.lib.gpb_set_stream(self.ctx, cuda_stream or None))
+
+    def copy_best(self, dst_ptr: int):
+        """D2D copy of the 16-byte gpb_best to a device address (async)."""
+        self._check(self.lib.gpb_copy_best(self.ctx, dst_ptr))
+
     def device_best_ptr(self) -> int:
         return self.lib.gpb_device_best(self.ctx)
 
@@ -171,6 +182,11 @@ class Planner:
         t = abi.Timing()
         self._check(self.lib.gpb_get_timing(self.ctx, C.byref(t)))
         return t
+
+    def microbench(self, kind: int = 0) -> float:
+        g = C.c_double()
+        self._check(self.lib.gpb_microbench(self.ctx, kind, C.byref(g)))
+        return g.value
 
     # ------------------------------------------------- reference mirrors
     def select(self, topos, scenario) -> SelectionReport:
