@@ -220,7 +220,8 @@ def impl_ours(args):
         dist.init_process_group("nccl")
     device = local if world > 1 else 0
     torch.cuda.set_device(device)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # one non-default stream for every launch and event
+    torch.cuda.set_stream(stream)
 
     topos, scens = workloads.config2(args.rows, seed=1 + rank)
     tarr = abi.array(abi.Topology, topos)

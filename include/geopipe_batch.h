@@ -254,6 +254,10 @@ int gpb_get_timing(gpb_ctx* ctx, gpb_timing* out);
  * register chains over every SM. Returns Gop/s. */
 int gpb_microbench(gpb_ctx* ctx, int32_t kind, double* gops);
 
+/* Profiling: record each row's clock64 cost in the evaluation kernels. */
+int gpb_set_profile(gpb_ctx* ctx, int32_t enable);
+int gpb_fetch_row_cycles(gpb_ctx* ctx, int64_t* out, int64_t n);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -1,0 +1,48 @@
+// atlas_layout.h — per-warp shared-memory slice of the ATLAS kernel, shared
+// by the host (sizing) and the device (carving). All offsets in bytes,
+// 16-byte aligned.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace gpb {
+
+struct AtlasLayout {
+  // inputs
+  int C, S, M, nw;     // nw = max WAN boundaries (<= 7)
+  bool garr_in_smem;
+  // outputs
+  size_t off_wa, off_wg, off_wbs, off_gf, off_cand, off_lastc, off_nm, off_done,
+      off_firstm, off_pub_nm, off_pub_last, off_pub_done, off_fdl, off_resf, off_resb,
+      off_garr, total;
+  int cap;             // list storage per WAN boundary = C * M (C lists of M)
+
+  __host__ __device__ static size_t al(size_t x) { return (x + 15) & ~(size_t)15; }
+
+  __host__ __device__ void compute() {
+    const size_t CS = (size_t)C * S;
+    cap = C * M;
+    size_t o = 0;
+    off_wa = o;        o = al(o + 8 * 8);
+    off_wg = o;        o = al(o + 8 * 8);
+    off_wbs = o;       o = al(o + (size_t)S * 4);   // WAN boundary before stage s
+    off_gf = o;        o = al(o + CS * 8);
+    off_cand = o;      o = al(o + CS * 8);
+    off_lastc = o;     o = al(o + (size_t)S * 8);
+    off_nm = o;        o = al(o + CS * 4);
+    off_done = o;      o = al(o + (size_t)S * 4);
+    off_firstm = o;    o = al(o + CS * 4);
+    off_pub_nm = o;    o = al(o + (size_t)C * 32 * 4);
+    off_pub_last = o;  o = al(o + 32 * 8);
+    off_pub_done = o;  o = al(o + 32 * 4);
+    off_fdl = o;       o = al(o + (size_t)C * M * 8);
+    off_resf = o;      o = al(o + (size_t)nw * cap * 8);
+    off_resb = o;      o = al(o + (size_t)nw * cap * 8);
+    off_garr = o;
+    if (garr_in_smem) o = al(o + CS * M * 8);
+    total = o;
+  }
+};
+
+}  // namespace gpb

@@ -135,6 +135,8 @@ static void validate_topology(const gpb_topology& t, int idx) {
   }
 }
 
+static std::string P_(int i) { return "scenarios[" + std::to_string(i) + "]"; }
+
 static int64_t act_bytes(const gpb_scenario& s) {
   return s.microbatch * s.seq_len * s.hidden * (int64_t)s.bytes_per_element;
 }
@@ -178,8 +180,6 @@ static void validate_scenario(const gpb_scenario& s, int idx, int n_topo,
   const int S = (s.num_layers + s.layers_per_partition - 1) / s.layers_per_partition;
   if (S > 256)
     throw ConfigErr{P + ": more than 256 pipeline stages is outside the kernel envelope"};
-  if (s.policy == GPB_ATLAS && (long long)s.pipelines_per_cell * S > 4096)
-    throw ConfigErr{P + ": atlas with C*S > 4096 is outside the kernel envelope"};
   if (act_bytes(s) <= 0) throw ConfigErr{"model: activation size overflow"};
 }
 
@@ -282,6 +282,13 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
         d.bwd_ms = s.bwd_ms;
         d.rec_ms = s.recompute_ms;
       }
+      if (d.policy == GPB_ATLAS) {
+        // the per-stage drain decomposition needs a positive pair duration
+        const long long dur = (long long)std::llround(d.bwd_ms * 1e6) +
+                              (d.recompute ? (long long)std::llround(d.rec_ms * 1e6) : 0);
+        if (dur <= 0)
+          throw ConfigErr{P_(i) + ": atlas pair duration rounds to 0 ns (outside the envelope)"};
+      }
       int order[GPB_MAX_DC];
       int n_order = s.n_order;
       if (n_order > 0) {
@@ -337,6 +344,9 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
       b.max_cs = std::max(b.max_cs, ds[i].C * ds[i].S);
       b.max_cm = std::max(b.max_cm, ds[i].C * ds[i].M);
       b.max_csm = std::max(b.max_csm, (long long)ds[i].C * ds[i].S * ds[i].M);
+      b.max_c = std::max(b.max_c, ds[i].C);
+      b.max_s = std::max(b.max_s, ds[i].S);
+      b.max_nw = std::max(b.max_nw, ds[i].n_order - 1);
     }
     b.count = (int32_t)work.size() - b.offset;
     c.buckets.push_back(b);
@@ -411,6 +421,8 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     a.cursor = cursors + bi;
     a.rows = (gpb_row*)c.b_rows.ptr;
     a.error_flag = err_flag;
+    a.row_cycles = c.profile_rows ? (long long*)c.dev_buf(c.b_cycles, 8 * (size_t)c.n_rows)
+                                  : nullptr;
     const int grid = std::min(grid_eval, (b.count + 3) / 4);
     cudaError_t e;
     if (b.policy == GPB_GPIPE || b.policy == GPB_VARUNA) {
@@ -424,22 +436,40 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     } else if (b.policy == GPB_1F1B) {
       e = launch_onef1b(b.B, a, grid, st);
     } else {
-      a.smem_cs = b.max_cs;
-      a.smem_warp_bytes = (int32_t)(((size_t)16 * 8 + (size_t)b.max_cs * 20 + 15) / 16 * 16);
-      if ((size_t)a.smem_warp_bytes * (kEvalThreads / 32) > (size_t)c.smem_optin) {
-        c.set_error("atlas C*S too large for the shared slice");
+      // per-warp shared slice. ATLAS rows are latency-bound per warp and the
+      // longest row sets the kernel time, so the gradient queues stay in
+      // shared memory whenever 4 warps per SM still fit (measured faster than
+      // higher occupancy with L1/L2-resident queues), else they go global.
+      AtlasLayout L;
+      L.C = b.max_c;
+      L.S = b.max_s;
+      L.M = b.max_m;
+      L.nw = b.max_nw;
+      L.garr_in_smem = true;
+      L.compute();
+      const size_t sm_budget = 220 * 1024;
+      if (L.total * 4 > sm_budget) {
+        L.garr_in_smem = false;
+        L.compute();
+      }
+      int wpc = (int)std::min<size_t>(4, (size_t)c.smem_optin / L.total);
+      if (wpc < 1) {
+        c.set_error("atlas plan too large for the shared-memory slice");
         return GPB_CONFIG_ERROR;
       }
-      a.res_cap = b.max_cm;
-      a.scratch_csm = b.max_csm;
-      a.scratch_cm = b.max_cm;
-      a.scratch_per_warp = b.max_csm + b.max_cm + 2LL * (GPB_MAX_DC - 1) * b.max_cm;
-      const int agrid = std::min(grid, c.num_sms * 8);
-      void* scr = c.dev_buf(c.b_scratch, sizeof(long long) * a.scratch_per_warp *
-                                             (size_t)agrid * (kEvalThreads / 32));
-      if (!scr) return c.cuda_fail(cudaErrorMemoryAllocation, "atlas scratch");
-      a.scratch = (long long*)scr;
-      e = launch_atlas(a, agrid, st);
+      a.lay = L;
+      const int per_sm = std::max(1, (int)std::min<size_t>(64 / wpc, sm_budget / (L.total * wpc)));
+      const int agrid = std::min(c.num_sms * per_sm, (b.count + wpc - 1) / wpc);
+      a.scratch = nullptr;
+      a.scratch_per_warp = 0;
+      if (!L.garr_in_smem) {
+        a.scratch_per_warp = (long long)L.C * L.S * L.M;
+        void* scr = c.dev_buf(c.b_scratch, sizeof(long long) * a.scratch_per_warp *
+                                               (size_t)agrid * wpc);
+        if (!scr) return c.cuda_fail(cudaErrorMemoryAllocation, "atlas scratch");
+        a.scratch = (long long*)scr;
+      }
+      e = launch_atlas(b.B, a, agrid, wpc, st);
     }
     if (e != cudaSuccess) return c.cuda_fail(e, "eval launch");
     ++launches;
@@ -597,4 +627,25 @@ extern "C" int gpb_microbench(gpb_ctx* ctx_, int32_t kind, double* gops) {
   *gops = ops / (best * 1e-3) / 1e9;
   c.timing_valid = false;
   return GPB_OK;
+}
+
+extern "C" int gpb_set_profile(gpb_ctx* ctx_, int32_t enable) {
+  if (!ctx_) return GPB_ERROR;
+  reinterpret_cast<Ctx*>(ctx_)->profile_rows = enable != 0;
+  return GPB_OK;
+}
+
+extern "C" int gpb_fetch_row_cycles(gpb_ctx* ctx_, int64_t* out, int64_t n) {
+  if (!ctx_ || !out) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  if (!c.profile_rows || !c.b_cycles.ptr) {
+    c.set_error("row profiling not enabled");
+    return GPB_CONFIG_ERROR;
+  }
+  cudaSetDevice(c.device);
+  n = std::min(n, c.n_rows);
+  cudaError_t e = cudaMemcpyAsync(out, c.b_cycles.ptr, 8 * (size_t)n, cudaMemcpyDeviceToHost,
+                                  c.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+  return e == cudaSuccess ? GPB_OK : c.cuda_fail(e, "fetch row cycles");
 }

@@ -26,6 +26,7 @@ struct Bucket {
   int max_cs = 0;
   int max_cm = 0;
   long long max_csm = 0;
+  int max_c = 0, max_s = 0, max_nw = 0;
 };
 
 struct Ctx {
@@ -51,7 +52,8 @@ struct Ctx {
 
   // device tables
   Buf b_topos, b_scens, b_row_scen, b_work, b_rows, b_results, b_cursors, b_best;
-  Buf b_scratch;
+  Buf b_scratch, b_cycles;
+  bool profile_rows = false;
   // timeline / bubbletea buffers
   Buf b_tl_rows, b_tl_spans, b_tl_nspan, b_tl_scratch, b_gaps, b_ngaps, b_reqs, b_pl,
       b_sum, b_pack_scratch, b_pack_misc;
@@ -63,7 +65,7 @@ struct Ctx {
 
   std::vector<Buf*> all_bufs() {
     return {&b_topos, &b_scens, &b_row_scen, &b_work, &b_rows, &b_results, &b_cursors,
-            &b_best, &b_scratch, &b_tl_rows, &b_tl_spans, &b_tl_nspan, &b_tl_scratch,
+            &b_best, &b_scratch, &b_cycles, &b_tl_rows, &b_tl_spans, &b_tl_nspan, &b_tl_scratch,
             &b_gaps, &b_ngaps, &b_reqs, &b_pl, &b_sum, &b_pack_scratch, &b_pack_misc};
   }
 

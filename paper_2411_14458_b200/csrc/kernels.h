@@ -7,6 +7,7 @@
 #include <cstdint>
 
 #include "../../include/geopipe_batch.h"
+#include "atlas_layout.h"
 
 namespace gpb {
 
@@ -24,16 +25,13 @@ struct EvalArgs {
   int32_t* cursor;            // atomic work cursor (zeroed per launch)
   gpb_row* rows;              // output table
   int32_t* error_flag;
+  long long* row_cycles;      // optional per-row clock64 cost (profiling)
   // flush: per-warp shared fd_last buffer length (max M of the bucket)
   int32_t smem_m;
-  // atlas: per-warp shared slice and global scratch layout
-  int32_t smem_cs;            // max C*S of the bucket
-  int32_t smem_warp_bytes;
-  int32_t res_cap;            // max C*M of the bucket
+  // atlas: per-warp shared slice and (when it does not fit) global garr
+  AtlasLayout lay;
   long long* scratch;
-  long long scratch_per_warp; // int64 elements
-  long long scratch_csm;      // max C*S*M
-  long long scratch_cm;       // max C*M
+  long long scratch_per_warp; // int64 elements per warp (global garr)
 };
 
 struct SelectArgs {
@@ -47,7 +45,7 @@ struct SelectArgs {
 
 cudaError_t launch_flush(int B, bool gpipe, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_onef1b(int B, const EvalArgs& a, int grid, cudaStream_t st);
-cudaError_t launch_atlas(const EvalArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_atlas(int B, const EvalArgs& a, int grid, int wpc, cudaStream_t st);
 cudaError_t launch_select(const SelectArgs& a, int grid, cudaStream_t st);
 
 }  // namespace gpb

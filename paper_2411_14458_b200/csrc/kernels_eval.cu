@@ -20,97 +20,9 @@
 // throughput, utilization).
 #include <cuda_runtime.h>
 
-#include "device_common.cuh"
-#include "kernels.h"
+#include "eval_common.cuh"
 
 namespace gpb {
-
-constexpr unsigned kFull = 0xffffffffu;
-
-__device__ __forceinline__ long long shfl_up64(long long v, int d) {
-  return __shfl_up_sync(kFull, v, d);
-}
-__device__ __forceinline__ long long shfl_down64(long long v, int d) {
-  return __shfl_down_sync(kFull, v, d);
-}
-__device__ __forceinline__ long long warp_max64(long long v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = imax(v, __shfl_xor_sync(kFull, v, o));
-  return v;
-}
-
-// Pull the next work item for this warp (lane 0 bumps the cursor).
-__device__ __forceinline__ int next_work(int* cursor) {
-  int idx = 0;
-  if ((threadIdx.x & 31) == 0) idx = atomicAdd(cursor, 1);
-  return __shfl_sync(kFull, idx, 0);
-}
-
-// Row header: decode + infeasible fast path. Returns false if infeasible.
-__device__ __forceinline__ bool begin_row(const EvalArgs& a, int row, Geom& g,
-                                          const DevScen*& sc, const DevTopo*& tp) {
-  const int si = a.row_scen[row];
-  sc = &a.scens[si];
-  tp = &a.topos[sc->topo];
-  const int d = (int)(row - sc->first_row) + 1;
-  decode(*sc, *tp, d, g);
-  if (!g.feasible) {
-    if ((threadIdx.x & 31) == 0) {
-      gpb_row r;
-      infeasible_row(r);
-      r.scenario = si;
-      r.d = d;
-      a.rows[row] = r;
-    }
-    return false;
-  }
-  return true;
-}
-
-__device__ __forceinline__ void end_row(const EvalArgs& a, int row, const Geom& g,
-                                        const DevScen& sc, const DevTopo& tp,
-                                        long long makespan, int err) {
-  if ((threadIdx.x & 31) == 0) {
-    gpb_row r;
-    infeasible_row(r);
-    r.scenario = a.row_scen[row];
-    r.d = g.D;
-    finish_row(sc, tp, g, makespan, r);
-    if (err) {
-      r.feasible = -1;  // kernel-side invariant failure: host raises GPB_ERROR
-      atomicExch(a.error_flag, 1);
-    }
-    a.rows[row] = r;
-  }
-}
-
-// Per-stage boundary info for the stages a lane owns.
-template <int B>
-struct StageLinks {
-  unsigned wanf = 0, wanb = 0;  // bit j: WAN boundary after / before stage
-  long long serf[B], latf[B], serb[B], latb[B];
-
-  __device__ __forceinline__ void load(const Geom& g, int lane, bool pooled) {
-#pragma unroll
-    for (int j = 0; j < B; ++j) {
-      const int s = lane * B + j;
-      serf[j] = latf[j] = serb[j] = latb[j] = 0;
-      int w;
-      if (s < g.S) {
-        if (s + 1 < g.S && wan_after(g, s, w)) {
-          wanf |= 1u << j;
-          serf[j] = pooled ? g.ser_pooled[w] : g.ser_spatial[w];
-          latf[j] = g.lat[w];
-        }
-        if (s > 0 && wan_after(g, s - 1, w)) {
-          wanb |= 1u << j;
-          serb[j] = pooled ? g.ser_pooled[w] : g.ser_spatial[w];
-          latb[j] = g.lat[w];
-        }
-      }
-    }
-  }
-};
 
 // ---------------------------------------------------------------- flush
 
@@ -196,12 +108,13 @@ __global__ void __launch_bounds__(kEvalThreads) flush_kernel(EvalArgs a) {
     const int w = next_work(a.cursor);
     if (w >= a.n_work) break;
     const int row = a.work[w];
+    const long long t_start = clock64();
     Geom g;
     const DevScen* sc;
     const DevTopo* tp;
     if (!begin_row(a, row, g, sc, tp)) continue;
     const long long mk = flush_row<B, GPIPE>(g, fdl);
-    end_row(a, row, g, *sc, *tp, mk, 0);
+    end_row(a, row, g, *sc, *tp, mk, 0, t_start);
     __syncwarp();
   }
 }
@@ -327,396 +240,14 @@ __global__ void __launch_bounds__(kEvalThreads) onef1b_kernel(EvalArgs a) {
     const int w = next_work(a.cursor);
     if (w >= a.n_work) break;
     const int row = a.work[w];
+    const long long t_start = clock64();
     Geom g;
     const DevScen* sc;
     const DevTopo* tp;
     if (!begin_row(a, row, g, sc, tp)) continue;
     int err = 0;
     const long long mk = onef1b_row<B>(g, err);
-    end_row(a, row, g, *sc, *tp, mk, err);
-    __syncwarp();
-  }
-}
-
-// ---------------------------------------------------------------- ATLAS
-
-// ReservationList (base.h:63-124) over uniform-length intervals: only the
-// starts are stored (sorted, non-overlapping), `len` is the boundary's pooled
-// serialization time.
-
-// first index i with st[i] + len > x (first interval ending after x)
-__device__ __forceinline__ int resv_first_end_after(const long long* st, int n,
-                                                    long long len, long long x) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (st[mid] + len > x) hi = mid; else lo = mid + 1;
-  }
-  return lo;
-}
-
-// earliest_fit (base.h:75-84)
-__device__ __forceinline__ long long resv_earliest_fit(const long long* st, int n,
-                                                       long long lo, long long len) {
-  if (len <= 0) return lo;
-  long long t = lo;
-  for (int i = resv_first_end_after(st, n, len, lo); i < n; ++i) {
-    if (st[i] >= t + len) break;
-    t = st[i] + len;
-  }
-  return t;
-}
-
-// free_at (base.h:65-72)
-__device__ __forceinline__ bool resv_free_at(const long long* st, int n, long long start,
-                                             long long len) {
-  if (len <= 0) return true;
-  const int i = resv_first_end_after(st, n, len, start);
-  return !(i < n && st[i] < start + len);
-}
-
-// reserve (base.h:101-106): insert before the first start >= x. Warp-wide.
-__device__ __forceinline__ void resv_insert_warp(long long* st, int& n, long long x,
-                                                 long long len) {
-  if (len <= 0) return;
-  const int lane = threadIdx.x & 31;
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (st[mid] < x) lo = mid + 1; else hi = mid;
-  }
-  for (int base = n - 1; base >= lo; base -= 32) {
-    const int idx = base - lane;
-    long long v = 0;
-    if (idx >= lo) v = st[idx];
-    __syncwarp();
-    if (idx >= lo) st[idx + 1] = v;
-    __syncwarp();
-  }
-  if (lane == 0) st[lo] = x;
-  __syncwarp();
-  n += 1;
-}
-
-struct AtlasScratch {
-  long long* garr;   // [C][S][M]
-  long long* fdl;    // [C][M]
-  long long* resf;   // [nb-1][cap]
-  long long* resb;   // [nb-1][cap]
-  long long* ps;     // [C][S][M] pair starts (timeline variant only)
-  int cap;
-};
-
-struct AtlasShared {   // pointers into this warp's shared-memory slice
-  long long* wa;       // [GPB_MAX_DC] chain offset a_w of WAN producer stages
-  long long* wg;       // [GPB_MAX_DC] prefix max G_w of WAN producer stages
-  long long* gf;       // [C][S] gpu_free
-  long long* cand;     // [C][S] cached greedy candidate start
-  int* nm;             // [C][S] next_m (drained count during forwards)
-  // list lengths: kept in registers, updated identically by every lane
-  int nres_f[GPB_MAX_DC];
-  int nres_b[GPB_MAX_DC];
-};
-
-__device__ __forceinline__ int wan_before_idx(const Geom& g, int s) {
-  int w;
-  return (s > 0 && wan_after(g, s - 1, w)) ? w : -1;
-}
-
-// Candidate start for pair (p, s) at its next microbatch (INF if not ready):
-// atlas_pair_start(max(ready, gpu_free)) (scheduler.cpp:461-485, 287-294).
-__device__ __forceinline__ long long atlas_candidate(const Geom& g, const AtlasScratch& X,
-                                                     const AtlasShared& H, int p, int s) {
-  const int S = g.S, M = g.M;
-  const int m = H.nm[p * S + s];
-  if (m >= M) return kInf64;
-  long long ready;
-  if (s == S - 1) {
-    ready = X.fdl[(size_t)p * M + m];
-  } else {
-    if (H.nm[p * S + s + 1] <= m) return kInf64;  // gradient not produced
-    ready = X.garr[((size_t)p * S + s) * M + m];
-  }
-  const long long lo = imax(ready, H.gf[p * S + s]);
-  const int w = wan_before_idx(g, s);
-  if (w < 0) return lo;
-  const long long* st = X.resb + (size_t)w * X.cap;
-  return resv_earliest_fit(st, H.nres_b[w], lo + g.dur, g.ser_pooled[w]) - g.dur;
-}
-
-// Lane-local best over the candidates of the stages this lane owns.
-__device__ __forceinline__ void lane_best(const Geom& g, const AtlasShared& H, int lane,
-                                          int B, long long& bt, unsigned& brank) {
-  bt = kInf64;
-  brank = 0xffffffffu;
-  const int S = g.S, C = g.C;
-  for (int j = 0; j < B; ++j) {
-    const int s = lane * B + j;
-    if (s >= S) break;
-    for (int p = 0; p < C; ++p) {
-      const long long t = H.cand[p * S + s];
-      const unsigned rank = (unsigned)((S - 1 - s) * C + p);  // scan order s desc, p asc
-      if (t < bt || (t == bt && rank < brank)) {
-        bt = t;
-        brank = rank;
-      }
-    }
-  }
-}
-
-template <bool TIMELINE>
-__device__ long long atlas_row(const Geom& g, int mem_limit, const AtlasScratch& X,
-                               AtlasShared& H, int& err) {
-  const int lane = threadIdx.x & 31;
-  const int S = g.S, M = g.M, C = g.C;
-  const int B = (S + 31) / 32;
-  const long long f = g.fwd, dur = g.dur;
-  for (int i = lane; i < C * S; i += 32) {
-    H.gf[i] = 0;
-    H.nm[i] = 0;
-  }
-  for (int w = 0; w < GPB_MAX_DC; ++w) H.nres_f[w] = H.nres_b[w] = 0;
-  __syncwarp();
-  // a_s = s*f + sum_{i<s} delta_i, delta_i = WAN ? ser_pooled + lat : 0:
-  // the chain offset of stage s.
-  // Lane-local prefix then warp exclusive scan.
-  long long a_loc[8];  // B <= 8 enforced on the host (S <= 256)
-  long long run = 0;
-  for (int j = 0; j < B; ++j) {
-    const int s = lane * B + j;
-    a_loc[j] = run;
-    if (s < S) {
-      run += f;
-      int w;
-      if (s + 1 < S && wan_after(g, s, w)) run += g.ser_pooled[w] + g.lat[w];
-    }
-  }
-  long long incl = run;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const long long v = shfl_up64(incl, o);
-    if (lane >= o) incl += v;
-  }
-  const long long excl = incl - run;
-  for (int j = 0; j < B; ++j) a_loc[j] += excl;
-
-  const int nw = g.nb - 1;  // WAN boundaries (ordinal w: producer stage blk_first[w+1]-1)
-
-  // ---------------- forward phase (scheduler.cpp:362-431)
-  for (int p = 0; p < C; ++p) {
-    for (int m = 0; m < M; ++m) {
-      // memory-cap admission with forced drains (atlas_drain_step)
-      for (;;) {
-        bool blk = false;
-        for (int j = 0; j < B; ++j) {
-          const int s = lane * B + j;
-          if (s < S && m - H.nm[p * S + s] >= mem_limit) blk = true;
-        }
-        if (!__any_sync(kFull, blk)) break;
-        // deepest stage with a ready pair
-        int my_s = -1;
-        for (int j = 0; j < B; ++j) {
-          const int s = lane * B + j;
-          if (s >= S) break;
-          const int dm = H.nm[p * S + s];
-          if (dm >= M) continue;
-          const bool ready = (s == S - 1) ? dm < m : H.nm[p * S + s + 1] > dm;
-          if (ready) my_s = s;
-        }
-        const unsigned bal = __ballot_sync(kFull, my_s >= 0);
-        if (bal == 0) {
-          err = 1;  // DeadlockError (cannot happen)
-          return 0;
-        }
-        const int src = 31 - __clz(bal);
-        const int s = __shfl_sync(kFull, my_s, src);
-        const int dm = H.nm[p * S + s];
-        const long long ready = (s == S - 1) ? X.fdl[(size_t)p * M + dm]
-                                             : X.garr[((size_t)p * S + s) * M + dm];
-        const long long lo = imax(ready, H.gf[p * S + s]);
-        const int w = wan_before_idx(g, s);
-        long long t = lo;
-        if (w >= 0) {
-          long long* st = X.resb + (size_t)w * X.cap;
-          t = resv_earliest_fit(st, H.nres_b[w], lo + dur, g.ser_pooled[w]) - dur;
-          int n = H.nres_b[w];
-          resv_insert_warp(st, n, t + dur, g.ser_pooled[w]);
-          H.nres_b[w] = n;
-        }
-        if (lane == 0) {
-          const long long e = t + dur;
-          H.gf[p * S + s] = imax(H.gf[p * S + s], e);
-          if (s > 0)
-            X.garr[((size_t)p * S + s - 1) * M + dm] =
-                w >= 0 ? e + g.ser_pooled[w] + g.lat[w] : e;
-          if (TIMELINE) X.ps[((size_t)p * S + s) * M + dm] = t;
-          H.nm[p * S + s] = dm + 1;
-        }
-        __syncwarp();
-      }
-      // chain fit: e_s(t0) = a_s + f + max(t0, G_s), G_s = max_{j<=s}(gf_j - a_j)
-      long long gl[8];
-      long long runmax = -kInf64;
-      for (int j = 0; j < B; ++j) {
-        const int s = lane * B + j;
-        if (s < S) runmax = imax(runmax, H.gf[p * S + s] - a_loc[j]);
-        gl[j] = runmax;
-      }
-      long long pre = runmax;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long v = shfl_up64(pre, o);
-        if (lane >= o) pre = imax(pre, v);
-      }
-      long long prev = shfl_up64(pre, 1);
-      if (lane == 0) prev = -kInf64;
-      for (int j = 0; j < B; ++j) gl[j] = imax(gl[j], prev);
-      // gather (a_w, G_w) of each WAN producer stage to every lane via smem
-      for (int j = 0; j < B; ++j) {
-        const int s = lane * B + j;
-        if (s < S) {
-          int w;
-          if (s + 1 < S && wan_after(g, s, w)) {
-            H.wa[w] = a_loc[j];
-            H.wg[w] = gl[j];
-          }
-        }
-      }
-      __syncwarp();
-      long long t0 = H.gf[p * S + 0];
-      if (lane == 0) {
-        for (;;) {
-          bool ok = true;
-          for (int w = 0; w < nw; ++w) {
-            const long long e = H.wa[w] + f + imax(t0, H.wg[w]);
-            const long long* st = X.resf + (size_t)w * X.cap;
-            const long long len = g.ser_pooled[w];
-            if (!resv_free_at(st, H.nres_f[w], e, len)) {
-              const long long slot = resv_earliest_fit(st, H.nres_f[w], e, len);
-              t0 += slot - e;
-              ok = false;
-              break;
-            }
-          }
-          if (ok) break;
-        }
-      }
-      t0 = __shfl_sync(kFull, t0, 0);
-      // commit the chain
-      for (int w = 0; w < nw; ++w) {
-        const long long e = H.wa[w] + f + imax(t0, H.wg[w]);
-        long long* st = X.resf + (size_t)w * X.cap;
-        int n = H.nres_f[w];
-        resv_insert_warp(st, n, e, g.ser_pooled[w]);
-        H.nres_f[w] = n;
-      }
-      for (int j = 0; j < B; ++j) {
-        const int s = lane * B + j;
-        if (s < S) {
-          const long long e = a_loc[j] + f + imax(t0, gl[j]);
-          H.gf[p * S + s] = e;
-          if (s == S - 1) X.fdl[(size_t)p * M + m] = e;
-        }
-      }
-      __syncwarp();
-    }
-  }
-
-  // ---------------- drain pass 1: greedy exact-fit (scheduler.cpp:452-505)
-  for (int i = lane; i < C * S; i += 32) H.cand[i] = 0;
-  __syncwarp();
-  long long remaining = 0;
-  for (int i = 0; i < C * S; ++i) remaining += M - H.nm[i];
-  for (int j = 0; j < B; ++j) {
-    const int s = lane * B + j;
-    if (s >= S) break;
-    for (int p = 0; p < C; ++p) H.cand[p * S + s] = atlas_candidate(g, X, H, p, s);
-  }
-  __syncwarp();
-  long long lbt;
-  unsigned lrank;
-  lane_best(g, H, lane, B, lbt, lrank);
-  while (remaining > 0) {
-    // warp argmin of (t, rank): three redux.sync steps on 32-bit parts
-    const unsigned hi = (unsigned)((unsigned long long)lbt >> 32);
-    const unsigned mh = __reduce_min_sync(kFull, hi);
-    const unsigned lo32 = hi == mh ? (unsigned)lbt : 0xffffffffu;
-    const unsigned ml = __reduce_min_sync(kFull, lo32);
-    const unsigned rk = (hi == mh && (unsigned)lbt == ml) ? lrank : 0xffffffffu;
-    const unsigned mr = __reduce_min_sync(kFull, rk);
-    const long long bt = (long long)(((unsigned long long)mh << 32) | ml);
-    if (bt >= kInf64 || mr == 0xffffffffu) {
-      err = 1;  // no ready candidate: cannot happen (last stage always ready)
-      return 0;
-    }
-    const int bs = S - 1 - (int)(mr / C), bp = (int)(mr % C);
-    const int bm = H.nm[bp * S + bs];
-    const int w = wan_before_idx(g, bs);
-    if (w >= 0) {
-      long long* st = X.resb + (size_t)w * X.cap;
-      int n = H.nres_b[w];
-      resv_insert_warp(st, n, bt + dur, g.ser_pooled[w]);
-      H.nres_b[w] = n;
-    }
-    if (lane == 0) {
-      H.gf[bp * S + bs] = bt + dur;
-      if (bs > 0)
-        X.garr[((size_t)bp * S + bs - 1) * M + bm] =
-            w >= 0 ? bt + dur + g.ser_pooled[w] + g.lat[w] : bt + dur;
-      if (TIMELINE) X.ps[((size_t)bp * S + bs) * M + bm] = bt;
-      H.nm[bp * S + bs] = bm + 1;
-    }
-    __syncwarp();
-    // refresh the candidates that changed: stage bs (all p when its
-    // gradient link is shared, else bp) and (bp, bs-1).
-    const int owner = bs / B, owner2 = bs > 0 ? (bs - 1) / B : -1;
-    if (lane == owner) {
-      if (w >= 0) {
-        for (int p = 0; p < C; ++p) H.cand[p * S + bs] = atlas_candidate(g, X, H, p, bs);
-      } else {
-        H.cand[bp * S + bs] = atlas_candidate(g, X, H, bp, bs);
-      }
-    }
-    __syncwarp();
-    if (lane == owner2) H.cand[bp * S + bs - 1] = atlas_candidate(g, X, H, bp, bs - 1);
-    __syncwarp();
-    if (lane == owner || lane == owner2) lane_best(g, H, lane, B, lbt, lrank);
-    --remaining;
-  }
-  long long mk = 0;
-  for (int i = lane; i < C * S; i += 32) mk = imax(mk, H.gf[i]);
-  return warp_max64(mk);
-}
-
-__global__ void __launch_bounds__(kEvalThreads) atlas_kernel(EvalArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x >> 5;
-  const int gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
-  unsigned char* base = smem + (size_t)warp * a.smem_warp_bytes;
-  AtlasShared H;
-  H.wa = reinterpret_cast<long long*>(base);
-  H.wg = H.wa + GPB_MAX_DC;
-  H.gf = H.wg + GPB_MAX_DC;
-  H.cand = H.gf + a.smem_cs;
-  H.nm = reinterpret_cast<int*>(H.cand + a.smem_cs);
-  AtlasScratch X;
-  X.cap = a.res_cap;
-  X.garr = a.scratch + (size_t)gwarp * a.scratch_per_warp;
-  X.fdl = X.garr + a.scratch_csm;
-  X.resf = X.fdl + a.scratch_cm;
-  X.resb = X.resf + (size_t)(GPB_MAX_DC - 1) * a.res_cap;
-  X.ps = nullptr;
-  for (;;) {
-    const int wk = next_work(a.cursor);
-    if (wk >= a.n_work) break;
-    const int row = a.work[wk];
-    Geom g;
-    const DevScen* sc;
-    const DevTopo* tp;
-    if (!begin_row(a, row, g, sc, tp)) continue;
-    int err = 0;
-    const long long mk = atlas_row<false>(g, sc->mem_limit, X, H, err);
-    end_row(a, row, g, *sc, *tp, mk, err);
+    end_row(a, row, g, *sc, *tp, mk, err, t_start);
     __syncwarp();
   }
 }
@@ -859,13 +390,6 @@ cudaError_t launch_onef1b(int B, const EvalArgs& a, int grid, cudaStream_t st) {
     case 8: onef1b_kernel<8><<<grid, kEvalThreads, 0, st>>>(a); break;
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
-}
-
-cudaError_t launch_atlas(const EvalArgs& a, int grid, cudaStream_t st) {
-  const size_t smem = (size_t)(kEvalThreads / 32) * a.smem_warp_bytes;
-  cudaFuncSetAttribute(atlas_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  atlas_kernel<<<grid, kEvalThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

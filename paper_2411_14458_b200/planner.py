@@ -76,6 +76,8 @@ def load_library(path: str = LIB_PATH):
         "gpb_microbench": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_double)]),
         "gpb_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
         "gpb_copy_best": (C.c_int, [C.c_void_p, C.c_void_p]),
+        "gpb_set_profile": (C.c_int, [C.c_void_p, C.c_int32]),
+        "gpb_fetch_row_cycles": (C.c_int, [C.c_void_p, P(C.c_int64), C.c_int64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -90,7 +92,7 @@ def exported_symbols():
             "gpb_load", "gpb_evaluate", "gpb_fetch_rows", "gpb_fetch_scenarios",
             "gpb_fetch_best", "gpb_device_best", "gpb_bubbles", "gpb_pack_prefills",
             "gpb_synthetic_requests", "gpb_get_timing", "gpb_microbench", "gpb_set_stream",
-            "gpb_copy_best"]
+            "gpb_copy_best", "gpb_set_profile", "gpb_fetch_row_cycles"]
 
 
 @dataclass
@@ -170,6 +172,14 @@ class Planner:
 
     def set_stream(self, cuda_stream: int | None):
         self._check(self.lib.gpb_set_stream(self.ctx, cuda_stream or None))
+
+    def set_profile(self, enable: bool):
+        self._check(self.lib.gpb_set_profile(self.ctx, int(bool(enable))))
+
+    def row_cycles(self):
+        out = (C.c_int64 * max(1, self.n_rows))()
+        self._check(self.lib.gpb_fetch_row_cycles(self.ctx, out, self.n_rows))
+        return list(out[: self.n_rows])
 
     def copy_best(self, dst_ptr: int):
         """D2D copy of the 16-byte gpb_best to a device address (async)."""

@@ -1,0 +1,34 @@
+"""Per-row clock64 cost of the evaluation kernels on a BASELINE workload,
+aggregated by (policy, S, C, M): where the device time goes."""
+import collections
+import json
+import sys
+
+sys.path.insert(0, ".")
+from paper_2411_14458_b200 import abi, workloads  # noqa: E402
+from paper_2411_14458_b200.planner import Planner  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "config2"
+topos, scens = getattr(workloads, cfg)()
+p = Planner(0)
+p.set_profile(True)
+n = p.load(abi.array(abi.Topology, topos), abi.array(abi.Scenario, scens))
+p.evaluate()
+p.evaluate()
+rows = p.rows()
+cyc = p.row_cycles()
+t = p.timing()
+agg = collections.defaultdict(lambda: [0, 0, 0])
+for r, c in zip(rows[:n], cyc):
+    s = scens[r.scenario]
+    S = (s.num_layers + s.layers_per_partition - 1) // s.layers_per_partition
+    key = (abi.POLICY_NAMES[s.policy], S, s.pipelines_per_cell, s.num_microbatches, r.feasible)
+    a = agg[key]
+    a[0] += 1
+    a[1] += c
+    a[2] = max(a[2], c)
+tot = sum(v[1] for v in agg.values())
+print(json.dumps({"evaluate_ms": t.evaluate_ms, "policy_ms": list(t.policy_ms)}))
+print("policy S C M feas | rows  sum_Mcyc  share  max_kcyc")
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:25]:
+    print(*k, "|", v[0], round(v[1] / 1e6, 2), f"{100 * v[1] / tot:.1f}%", round(v[2] / 1e3, 1))
