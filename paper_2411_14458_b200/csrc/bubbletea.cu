@@ -1,7 +1,835 @@
-// bubbletea.cu — bubbles and BubbleTea packing (filled in below).
+// bubbletea.cu — bubbles (extract_bubbles, bubbletea.cpp:20-66) and
+// BubbleTea prefill packing (build_prefill_pipelines + schedule_prefills,
+// bubbletea.cpp:88-222) for a set of plan rows, on sm_100a.
+//
+// 1. timeline kernels (kernels_eval.cu / kernels_atlas.cu) write forward
+//    ends and pair starts per (pipeline, stage, microbatch) of cell 0 (all D
+//    cells are identical; for gpipe/1f1b/varuna so are the pipelines);
+// 2. gap_kernel: one thread per (row, pipeline, stage) merges forwards and
+//    pairs in start order, clips to the horizon and emits gaps_of()'s gap
+//    list with the before-training flags;
+// 3. pack_kernel: one warp per row runs the FCFS request loop. For each
+//    request the 32 lanes each take a prefill pipeline (first-fit = lowest
+//    index: ballot + ffs) and find its earliest common start t0 >= arrival by
+//    a leapfrog over the D stage GPUs: a stage that does not fit at t bumps t
+//    to the next gap start (minus its offset) that can hold it. The minimum
+//    feasible t0 over the reals is always one of the reference's candidates
+//    ({arrival} U {gap.start - off_k}), so the first feasible candidate the
+//    reference finds is exactly this minimum. The winning lane set commits
+//    the split of each stage's gap (copy-on-write per GPU list).
 #include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
 #include "../../include/geopipe_batch.h"
+#include "eval_common.cuh"
 #include "host_internal.h"
-extern "C" int gpb_bubbles(gpb_ctx*, int64_t, int64_t, gpb_bubble*, int64_t, int64_t*) { return GPB_ERROR; }
-extern "C" int gpb_pack_prefills(gpb_ctx*, const int64_t*, int32_t, const gpb_request*, int64_t,
-                                 const gpb_prefill_model*, int64_t, gpb_pack_summary*, gpb_placement*) { return GPB_ERROR; }
+
+namespace gpb {
+
+// Per-row descriptor of a timeline / packing slot.
+struct TlSlot {
+  long long row;
+  long long tl_off;   // into fe / ps  ([Ce][S][M])
+  long long gap_off;  // into gap arrays ([Ce][S][2M+1])
+  long long lst_off;  // into per-list arrays ([Ce][S])
+  long long horizon;  // <= 0: makespan of the row
+  long long fwd, dur;
+  int S, M, Ce, C, D, policy;
+};
+
+__device__ __forceinline__ unsigned long long fnv_mix(unsigned long long h, unsigned long long v) {
+  for (int i = 0; i < 8; ++i) {
+    h ^= (v >> (8 * i)) & 0xffu;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+__global__ void gap_kernel(const TlSlot* slots, int n_slots, const gpb_row* tl_rows,
+                           const long long* fe, const long long* ps, long long* glo,
+                           long long* ghi, unsigned char* gflag, int* gcnt,
+                           long long* gsum, int* ghas, long long* hz_out) {
+  // grid.y = slot, threads over its (pipeline, stage) lists
+  const int si = blockIdx.y;
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (si >= n_slots) return;
+  const TlSlot& sl = slots[si];
+  if (gid >= (long long)sl.Ce * sl.S) return;
+  const int M = sl.M;
+  const int li = (int)gid;  // = p * S + s
+  const long long H = sl.horizon > 0 ? sl.horizon : tl_rows[sl.row].makespan_ns;
+  if (li == 0) hz_out[si] = H;
+  const long long* F = fe + sl.tl_off + (size_t)li * M;
+  const long long* P = ps + sl.tl_off + (size_t)li * M;
+  long long* lo_out = glo + sl.gap_off + (size_t)li * (2 * M + 1);
+  long long* hi_out = ghi + sl.gap_off + (size_t)li * (2 * M + 1);
+  unsigned char* fl_out = gflag + sl.gap_off + (size_t)li * (2 * M + 1);
+  const bool rev = sl.policy == GPB_GPIPE;  // gpipe drains in reverse order
+  int i_f = 0, i_p = 0, n = 0, has = 0;
+  long long cursor = 0, sum = 0;
+  while (i_f < M || i_p < M) {
+    long long fs = kInf64, pst = kInf64;
+    if (i_f < M) fs = F[i_f] - sl.fwd;
+    if (i_p < M) pst = P[rev ? M - 1 - i_p : i_p];
+    long long lo, hi;
+    if (fs <= pst) {
+      lo = fs;
+      hi = fs + sl.fwd;
+      ++i_f;
+    } else {
+      lo = pst;
+      hi = pst + sl.dur;
+      ++i_p;
+    }
+    lo = imax(lo, 0);  // busy_by_gpu clipping (bubbletea.cpp:24-26)
+    hi = imin(hi, H);
+    if (lo >= hi) continue;
+    has = 1;
+    if (lo > cursor) {  // gaps_of (bubbletea.cpp:44-53)
+      lo_out[n] = cursor;
+      hi_out[n] = lo;
+      fl_out[n] = 1;  // the next span is a training task
+      sum += lo - cursor;
+      ++n;
+    }
+    cursor = imax(cursor, hi);
+  }
+  if (cursor < H) {
+    lo_out[n] = cursor;
+    hi_out[n] = H;
+    fl_out[n] = 0;
+    sum += H - cursor;
+    ++n;
+  }
+  gcnt[sl.lst_off + li] = n;
+  gsum[sl.lst_off + li] = sum;
+  ghas[sl.lst_off + li] = has;
+}
+
+// ------------------------------------------------------------ packing
+
+struct PackArgs {
+  const TlSlot* slots;
+  int n_slots;
+  const DevScen* scens;
+  const DevTopo* topos;
+  const int32_t* row_scen;
+  const long long* glo;
+  const long long* ghi;
+  const unsigned char* gflag;
+  const int* gcnt;
+  const long long* gsum;
+  const long long* hz;
+  const gpb_request* reqs;
+  long long n_req;
+  long long first_late_req_dummy;
+  // prefill model (PrefillModel, bubbletea.h:38-58), pre-validated
+  double sat_ms, stage_bw, lat_ms;
+  int max_tokens, inf_layers, bpe, pad_;
+  long long inf_hidden;
+  long long guard_ns;
+  // copy-on-write per-GPU lists
+  long long* pool_lo;
+  long long* pool_hi;
+  unsigned char* pool_fl;
+  long long pool_per_slot;
+  long long* gpu_off;       // [slot gpu base + gi]  -1 = shared
+  int* gpu_cnt;
+  int* gpu_cap;
+  const long long* gpu_base;  // per slot offset into gpu_* arrays
+  // outputs
+  gpb_pack_summary* sums;
+  gpb_placement* pl;        // nullable: [slot][req]
+  int* overflow;
+};
+
+struct ListView {
+  const long long* lo;
+  const long long* hi;
+  const unsigned char* fl;
+  int n;
+};
+
+__device__ __forceinline__ ListView view_of(const PackArgs& a, const TlSlot& sl, long long gb,
+                                            int gi, int li_shared) {
+  ListView v;
+  const long long off = a.gpu_off[gb + gi];
+  if (off >= 0) {
+    v.lo = a.pool_lo + off;
+    v.hi = a.pool_hi + off;
+    v.fl = a.pool_fl + off;
+    v.n = a.gpu_cnt[gb + gi];
+  } else {
+    const long long go = sl.gap_off + (long long)li_shared * (2 * sl.M + 1);
+    v.lo = a.glo + go;
+    v.hi = a.ghi + go;
+    v.fl = a.gflag + go;
+    v.n = a.gcnt[sl.lst_off + li_shared];
+  }
+  return v;
+}
+
+// last index j with lo[j] <= x, or -1
+__device__ __forceinline__ int last_start_le(const ListView& v, long long x) {
+  int lo = 0, hi = v.n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (v.lo[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo - 1;
+}
+
+__device__ __forceinline__ long long usable_end(const ListView& v, int j, long long guard) {
+  return v.hi[j] - (v.fl[j] ? guard : 0);
+}
+
+// Gap that admits [lo, lo+dur) in the reference's scan (bubbletea.cpp:173-188):
+// the last gap starting at or before lo, or — for a zero-length interval —
+// the gap just before it when the two touch at lo. Returns -1 if none.
+__device__ __forceinline__ int fitting_gap(const ListView& v, long long lo, long long dur,
+                                           long long guard) {
+  const int j = last_start_le(v, lo);
+  if (j < 0) return -1;
+  if (lo + dur <= usable_end(v, j, guard)) return j;
+  if (dur == 0 && j >= 1 && v.hi[j - 1] == lo && usable_end(v, j - 1, guard) >= lo) return j - 1;
+  return -1;
+}
+
+// Smallest gap start > x that can start a [start, start+dur) placement.
+__device__ __forceinline__ long long next_start(const ListView& v, long long x, long long dur,
+                                                long long guard) {
+  for (int j = last_start_le(v, x) + 1; j < v.n; ++j) {
+    const long long st = v.lo[j];
+    if (st + dur <= usable_end(v, j, guard)) return st;
+    if (dur == 0 && j >= 1 && v.hi[j - 1] == st && usable_end(v, j - 1, guard) >= st) return st;
+  }
+  return kInf64;
+}
+
+struct ReqGeom {
+  long long d0, d1, ovh;
+  int extra;
+  __device__ __forceinline__ long long dur(int k) const { return k < extra ? d1 : d0; }
+  __device__ __forceinline__ long long off(int k) const {
+    return k <= extra ? (long long)k * (d1 + ovh)
+                      : (long long)extra * (d1 + ovh) + (long long)(k - extra) * (d0 + ovh);
+  }
+};
+
+__device__ __forceinline__ int gpu_index(int k, int pipe, int stage, int C, int S) {
+  return (k * C + pipe) * S + stage;
+}
+
+// Make GPU gi's list private with room for one more gap; returns false on
+// pool exhaustion.
+__device__ bool ensure_private(const PackArgs& a, const TlSlot& sl, long long gb, int gi,
+                               int li_shared, long long& bump, long long pool_base) {
+  long long off = a.gpu_off[gb + gi];
+  int n = off >= 0 ? a.gpu_cnt[gb + gi] : a.gcnt[sl.lst_off + li_shared];
+  int cap = off >= 0 ? a.gpu_cap[gb + gi] : 0;
+  if (off >= 0 && n + 1 <= cap) return true;
+  const int ncap = max(2 * cap, n + 8);
+  if (bump + ncap > a.pool_per_slot) return false;
+  const long long noff = pool_base + bump;
+  bump += ncap;
+  ListView v = view_of(a, sl, gb, gi, li_shared);
+  for (int j = 0; j < n; ++j) {
+    a.pool_lo[noff + j] = v.lo[j];
+    a.pool_hi[noff + j] = v.hi[j];
+    a.pool_fl[noff + j] = v.fl[j];
+  }
+  a.gpu_off[gb + gi] = noff;
+  a.gpu_cnt[gb + gi] = n;
+  a.gpu_cap[gb + gi] = ncap;
+  return true;
+}
+
+__global__ void __launch_bounds__(128) pack_kernel(PackArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int si = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (si >= a.n_slots) return;
+  const TlSlot& sl = a.slots[si];
+  const long long H = a.hz[si];
+  const int D = sl.D, C = sl.C, S = sl.S, Ce = sl.Ce;
+  const long long gb = a.gpu_base[si];
+  const int G = D * C * S;
+  for (int i = lane; i < G; i += 32) a.gpu_off[gb + i] = -1;
+  __syncwarp();
+  const long long pool_base = (long long)si * a.pool_per_slot;
+  long long bump = 0;
+  // build_prefill_pipelines (bubbletea.cpp:88-130): layers per cell
+  const int base_l = a.inf_layers / D, extra = a.inf_layers % D;
+  const int total_layers = max(1, base_l * D + extra);
+  long long accepted = 0, rejected = 0;
+  unsigned long long hash = 1469598103934665603ull;
+  const int n_pipes = C * S;
+  for (long long r = 0; r < a.n_req; ++r) {
+    const gpb_request q = a.reqs[r];
+    const long long arrival = ms_to_ns(q.arrival_ms);
+    int win = -1;
+    long long win_t = 0;
+    ReqGeom rg;
+    double xfer = 0.0;
+    if (arrival <= H) {
+      // prefill_duration_ms (:68-76), transfer (:78-86), stage durations (:154-161)
+      const double dur_ms = __ddiv_rn(__dmul_rn(a.sat_ms, (double)q.tokens), (double)a.max_tokens);
+      const double bytes = (double)((long long)q.tokens * a.inf_hidden * a.bpe);
+      xfer = __dadd_rn(a.lat_ms, __ddiv_rn(bytes, a.stage_bw));
+      rg.ovh = ms_to_ns(xfer);
+      rg.d1 = ms_to_ns(__ddiv_rn(__dmul_rn(dur_ms, (double)(base_l + 1)), (double)total_layers));
+      rg.d0 = ms_to_ns(__ddiv_rn(__dmul_rn(dur_ms, (double)base_l), (double)total_layers));
+      rg.extra = extra;
+      for (int c0 = 0; c0 < n_pipes && win < 0; c0 += 32) {
+        const int pi = c0 + lane;
+        long long t_found = kInf64;
+        if (pi < n_pipes) {
+          const int pipe = pi / S, stage = pi % S;
+          const int li = (Ce > 1 ? pipe : 0) * S + stage;
+          long long t = arrival;
+          int ok_run = 0, k = 0;
+          while (ok_run < D) {
+            const ListView v = view_of(a, sl, gb, gpu_index(k, pipe, stage, C, S), li);
+            const long long off = rg.off(k), dk = rg.dur(k);
+            if (fitting_gap(v, t + off, dk, a.guard_ns) >= 0) {
+              ++ok_run;
+            } else {
+              const long long st = next_start(v, t + off, dk, a.guard_ns);
+              if (st == kInf64) {
+                t = kInf64;
+                break;
+              }
+              t = st - off;
+              ok_run = 1;
+            }
+            k = k + 1 == D ? 0 : k + 1;
+          }
+          t_found = t;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, t_found != kInf64);
+        if (bal) {
+          const int src = __ffs(bal) - 1;
+          win = c0 + src;
+          win_t = __shfl_sync(0xffffffffu, t_found, src);
+        }
+      }
+    }
+    if (win >= 0) {
+      // commit (bubbletea.cpp:189-215): split the gap on each stage GPU
+      const int pipe = win / S, stage = win % S;
+      const int li = (Ce > 1 ? pipe : 0) * S + stage;
+      bool ovf = false;
+      // one lane commits (the per-warp bump allocator is serial); a
+      // zero-length interval at a gap end changes nothing (upper_bound
+      // insertion behind the span that ends the gap)
+      for (int k = 0; k < D && !ovf; ++k) {
+        const int gi = gpu_index(k, pipe, stage, C, S);
+        const long long lo = win_t + rg.off(k), hi = lo + rg.dur(k);
+        bool need = false;
+        if (lane == 0) {
+          const ListView v0 = view_of(a, sl, gb, gi, li);
+          const int j = fitting_gap(v0, lo, hi - lo, a.guard_ns);
+          need = j >= 0 && lo != v0.hi[j];
+          if (need && !ensure_private(a, sl, gb, gi, li, bump, pool_base)) ovf = true;
+          if (need && !ovf) {
+            long long* L = a.pool_lo + a.gpu_off[gb + gi];
+            long long* Hh = a.pool_hi + a.gpu_off[gb + gi];
+            unsigned char* Fl = a.pool_fl + a.gpu_off[gb + gi];
+            int n = a.gpu_cnt[gb + gi];
+            const long long glo = L[j], ghi = Hh[j];
+            const unsigned char gfl = Fl[j];
+            const int add_l = lo > glo, add_r = ghi > hi;
+            const int delta = add_l + add_r - 1;
+            if (delta > 0) {
+              for (int x = n - 1; x > j; --x) {
+                L[x + 1] = L[x];
+                Hh[x + 1] = Hh[x];
+                Fl[x + 1] = Fl[x];
+              }
+            } else if (delta < 0) {
+              for (int x = j + 1; x < n; ++x) {
+                L[x - 1] = L[x];
+                Hh[x - 1] = Hh[x];
+                Fl[x - 1] = Fl[x];
+              }
+            }
+            int w = j;
+            if (add_l) {
+              L[w] = glo;
+              Hh[w] = lo;
+              Fl[w] = 0;  // the next span is this prefill
+              ++w;
+            }
+            if (add_r) {
+              L[w] = hi;
+              Hh[w] = ghi;
+              Fl[w] = gfl;
+            }
+            a.gpu_cnt[gb + gi] = n + delta;
+          }
+        }
+        ovf = __shfl_sync(0xffffffffu, (int)ovf, 0);
+      }
+      if (ovf) {
+        if (lane == 0) atomicExch(a.overflow, 1);
+        return;
+      }
+      ++accepted;
+      if (lane == 0) {
+        hash = fnv_mix(hash, (unsigned long long)(long long)q.id);
+        hash = fnv_mix(hash, (unsigned long long)(long long)win);
+        hash = fnv_mix(hash, (unsigned long long)win_t);
+        if (a.pl) {
+          gpb_placement& o = a.pl[(size_t)si * a.n_req + r];
+          o.start_ns = win_t;
+          o.ttft_overhead_ms = D - 1 == 0 ? 0.0 : __dmul_rn((double)(D - 1), xfer);
+          o.accepted = 1;
+          o.pipeline = win;
+        }
+      }
+    } else {
+      ++rejected;
+      if (lane == 0 && a.pl) {
+        gpb_placement& o = a.pl[(size_t)si * a.n_req + r];
+        o.start_ns = -1;
+        o.ttft_overhead_ms = 0.0;
+        o.accepted = 0;
+        o.pipeline = -1;
+      }
+    }
+    __syncwarp();
+  }
+  // utilization before/after (bubbletea.cpp:224-238): per GPU busy = H - sum
+  // of its gaps, summed in GPU-id order (DC in topology order, then cell,
+  // pipeline, stage within the DC's block), then / G.
+  if (lane == 0) {
+    const int row = (int)sl.row;
+    const DevScen& sc = a.scens[a.row_scen[row]];
+    const DevTopo& tp = a.topos[sc.topo];
+    Geom g;
+    decode(sc, tp, sl.D, g);
+    double ub = 0.0, ua = 0.0;
+    for (int dc = 0; dc < tp.n_dc; ++dc) {
+      int b = -1;
+      for (int x = 0; x < g.nb; ++x)
+        if (g.blk_dc[x] == dc) b = x;
+      if (b < 0) continue;
+      for (int k = 0; k < D; ++k)
+        for (int pipe = 0; pipe < C; ++pipe)
+          for (int s = g.blk_first[b]; s < g.blk_first[b + 1]; ++s) {
+            const int li = (Ce > 1 ? pipe : 0) * S + s;
+            const long long bsum = a.gsum[sl.lst_off + li];
+            ub = __dadd_rn(ub, __ddiv_rn((double)(H - bsum), (double)H));
+            const int gi = gpu_index(k, pipe, s, C, S);
+            long long asum = bsum;
+            if (a.gpu_off[gb + gi] >= 0) {
+              asum = 0;
+              const long long o = a.gpu_off[gb + gi];
+              for (int x = 0; x < a.gpu_cnt[gb + gi]; ++x) asum += a.pool_hi[o + x] - a.pool_lo[o + x];
+            }
+            ua = __dadd_rn(ua, __ddiv_rn((double)(H - asum), (double)H));
+          }
+    }
+    gpb_pack_summary& o = a.sums[si];
+    o.utilization_before = __ddiv_rn(ub, (double)G);
+    o.utilization_after = __ddiv_rn(ua, (double)G);
+    o.accepted = accepted;
+    o.rejected = rejected;
+    o.horizon_ns = H;
+    o.placement_hash = hash;
+  }
+}
+
+}  // namespace gpb
+
+// ------------------------------------------------------------------ host
+
+using namespace gpb;
+
+namespace {
+
+struct HostBlocks {
+  int nb = 0;
+  int dc[GPB_MAX_DC];
+  int first[GPB_MAX_DC + 1];
+  bool feasible = false;
+};
+
+// build_plan's walk (workload.cpp:57-89) on the host, for GPU numbering.
+HostBlocks host_decode(const DevScen& sc, const DevTopo& t, int d) {
+  HostBlocks h;
+  int assigned = 0;
+  const int denom = d * sc.C * sc.tp;
+  for (int i = 0; i < sc.n_order; ++i) {
+    if (assigned >= sc.S) break;
+    const int dc = sc.order[i];
+    const int take = std::min(sc.S - assigned, t.gpu_count[dc] / denom);
+    if (take > 0) {
+      h.first[h.nb] = assigned;
+      h.dc[h.nb] = dc;
+      ++h.nb;
+      assigned += take;
+    }
+  }
+  h.first[h.nb] = assigned;
+  h.feasible = assigned >= sc.S;
+  return h;
+}
+
+long long host_ms_to_ns(double ms) { return std::llround(ms * 1e6); }
+
+// Runs the timeline kernels for `rows` and the gap kernel; fills slots.
+int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
+                    std::vector<TlSlot>& slots) {
+  cudaStream_t st = c.stream;
+  slots.resize(n);
+  long long tl = 0, gp = 0, ls = 0;
+  for (int i = 0; i < n; ++i) {
+    if (rows[i] < 0 || rows[i] >= c.n_rows) {
+      c.set_error("row index out of range");
+      return GPB_CONFIG_ERROR;
+    }
+    const int si = c.row_scen_host[rows[i]];
+    const DevScen& sc = c.dev_scens_host[si];
+    const DevTopo& tp = c.dev_topos_host[sc.topo];
+    const int d = (int)(rows[i] - sc.first_row) + 1;
+    HostBlocks hb = host_decode(sc, tp, d);
+    if (!hb.feasible) {
+      c.set_error("plan needs more GPUs than the topology (row %lld)", (long long)rows[i]);
+      return GPB_INFEASIBLE;
+    }
+    TlSlot& s = slots[i];
+    s.row = rows[i];
+    s.S = sc.S;
+    s.M = sc.M;
+    s.C = sc.C;
+    s.D = d;
+    s.policy = sc.policy;
+    s.Ce = sc.policy == GPB_ATLAS ? sc.C : 1;
+    s.fwd = host_ms_to_ns(sc.fwd_ms);
+    s.dur = host_ms_to_ns(sc.bwd_ms) + (sc.recompute ? host_ms_to_ns(sc.rec_ms) : 0);
+    s.horizon = horizon;
+    s.tl_off = tl;
+    s.gap_off = gp;
+    s.lst_off = ls;
+    tl += (long long)s.Ce * s.S * s.M;
+    gp += (long long)s.Ce * s.S * (2 * s.M + 1);
+    ls += (long long)s.Ce * s.S;
+  }
+  long long* fe = (long long*)c.dev_buf(c.b_tl_spans, 16 * (size_t)std::max(1LL, tl));
+  long long* ps = fe + std::max(1LL, tl);
+  gpb_row* tl_rows = (gpb_row*)c.dev_buf(c.b_tl_rows, sizeof(gpb_row) * (size_t)c.n_rows);
+  long long* glo = (long long*)c.dev_buf(c.b_gaps, 17 * (size_t)std::max(1LL, gp));
+  long long* ghi = glo + std::max(1LL, gp);
+  unsigned char* gfl = (unsigned char*)(ghi + std::max(1LL, gp));
+  int* gcnt = (int*)c.dev_buf(c.b_ngaps, 24 * (size_t)std::max(1LL, ls) + 8 * (size_t)n + 64);
+  long long* gsum = (long long*)(gcnt + 2 * std::max(1LL, ls));
+  int* ghas = (int*)(gsum + std::max(1LL, ls));
+  long long* hz = (long long*)(ghas + 2 * std::max(1LL, ls));
+  TlSlot* dslots = (TlSlot*)c.dev_buf(c.b_tl_nspan, sizeof(TlSlot) * (size_t)std::max(1, n));
+  if (!fe || !tl_rows || !glo || !gcnt || !dslots)
+    return c.cuda_fail(cudaErrorMemoryAllocation, "timeline buffers");
+  // per-(policy, B) work lists over the slots
+  std::vector<int32_t> work;
+  std::vector<long long> offs;
+  struct Grp {
+    int policy, B, off, cnt, max_m, max_c, max_s, max_nw;
+  };
+  std::vector<Grp> grps;
+  for (int pol = 0; pol < 4; ++pol)
+    for (int B = 1; B <= 8; ++B) {
+      Grp g{pol, B, (int)work.size(), 0, 0, 0, 0, 0};
+      for (int i = 0; i < n; ++i) {
+        const DevScen& sc = c.dev_scens_host[c.row_scen_host[rows[i]]];
+        if (sc.policy != pol || (sc.S + 31) / 32 != B) continue;
+        work.push_back((int32_t)rows[i]);
+        offs.push_back(slots[i].tl_off);
+        g.max_m = std::max(g.max_m, sc.M);
+        g.max_c = std::max(g.max_c, sc.C);
+        g.max_s = std::max(g.max_s, sc.S);
+        g.max_nw = std::max(g.max_nw, sc.n_order - 1);
+        ++g.cnt;
+      }
+      if (g.cnt) grps.push_back(g);
+    }
+  int32_t* dwork = (int32_t*)c.dev_buf(c.b_reqs, 4 * work.size() + 8 * offs.size() + 64);
+  long long* doffs = (long long*)(dwork + ((work.size() + 1) & ~(size_t)1));
+  int32_t* cursors = (int32_t*)c.dev_buf(c.b_pack_misc, 4 * (grps.size() + 2));
+  if (!dwork || !cursors) return c.cuda_fail(cudaErrorMemoryAllocation, "timeline work");
+  cudaMemcpyAsync(dwork, work.data(), 4 * work.size(), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(doffs, offs.data(), 8 * offs.size(), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(dslots, slots.data(), sizeof(TlSlot) * n, cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(cursors, 0, 4 * (grps.size() + 2), st);
+  for (size_t gi = 0; gi < grps.size(); ++gi) {
+    const Grp& g = grps[gi];
+    EvalArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.scens = (const DevScen*)c.b_scens.ptr;
+    a.topos = (const DevTopo*)c.b_topos.ptr;
+    a.row_scen = (const int32_t*)c.b_row_scen.ptr;
+    a.work = dwork + g.off;
+    a.n_work = g.cnt;
+    a.cursor = cursors + gi;
+    a.rows = tl_rows;
+    a.error_flag = cursors + grps.size();
+    a.tl_fe = fe;
+    a.tl_ps = ps;
+    a.tl_off = doffs + g.off;
+    cudaError_t e;
+    if (g.policy != GPB_ATLAS) {
+      a.smem_m = g.max_m;
+      e = launch_timeline(g.policy, g.B, a, std::min(c.num_sms * 8, (g.cnt + 3) / 4), st);
+    } else {
+      AtlasLayout L;
+      L.C = g.max_c;
+      L.S = g.max_s;
+      L.M = g.max_m;
+      L.nw = g.max_nw;
+      L.garr_in_smem = true;
+      L.compute();
+      if (L.total * 4 > 220 * 1024) {
+        L.garr_in_smem = false;
+        L.compute();
+      }
+      const int wpc = (int)std::min<size_t>(4, (size_t)c.smem_optin / L.total);
+      if (wpc < 1) {
+        c.set_error("atlas plan too large for the shared-memory slice");
+        return GPB_CONFIG_ERROR;
+      }
+      a.lay = L;
+      const int grid = std::min(c.num_sms * 4, (g.cnt + wpc - 1) / wpc);
+      if (!L.garr_in_smem) {
+        a.scratch_per_warp = (long long)L.C * L.S * L.M;
+        a.scratch = (long long*)c.dev_buf(c.b_tl_scratch,
+                                          8 * (size_t)a.scratch_per_warp * grid * wpc);
+        if (!a.scratch) return c.cuda_fail(cudaErrorMemoryAllocation, "atlas scratch");
+      }
+      e = launch_atlas_timeline(g.B, a, grid, wpc, st);
+    }
+    if (e != cudaSuccess) return c.cuda_fail(e, "timeline launch");
+  }
+  long long max_lists = 1;
+  for (const TlSlot& s : slots) max_lists = std::max(max_lists, (long long)s.Ce * s.S);
+  gap_kernel<<<dim3((unsigned)((max_lists + 127) / 128), (unsigned)n), 128, 0, st>>>(
+      dslots, n, tl_rows, fe, ps, glo, ghi, gfl, gcnt, gsum, ghas, hz);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return c.cuda_fail(e, "gap kernel");
+  int32_t flag = 0;
+  cudaMemcpyAsync(&flag, cursors + grps.size(), 4, cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return c.cuda_fail(e, "timelines");
+  if (flag) {
+    c.set_error("kernel invariant failure in the timeline kernels");
+    return GPB_ERROR;
+  }
+  c.tl_glo = glo;
+  c.tl_ghi = ghi;
+  c.tl_gfl = gfl;
+  c.tl_gcnt = gcnt;
+  c.tl_gsum = gsum;
+  c.tl_ghas = ghas;
+  c.tl_hz = hz;
+  c.tl_slots_dev = (void*)dslots;
+  return GPB_OK;
+}
+
+}  // namespace
+
+extern "C" int gpb_bubbles(gpb_ctx* ctx_, int64_t row, int64_t horizon_ns, gpb_bubble* out,
+                           int64_t cap, int64_t* n_out) {
+  if (!ctx_) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  c.last_error.clear();
+  if (!c.loaded) {
+    c.set_error("no plan space loaded");
+    return GPB_CONFIG_ERROR;
+  }
+  cudaSetDevice(c.device);
+  std::vector<TlSlot> slots;
+  int rc = build_timelines(c, &row, 1, horizon_ns, slots);
+  if (rc != GPB_OK) return rc;
+  const TlSlot& s = slots[0];
+  const size_t nl = (size_t)s.Ce * s.S, per = 2 * (size_t)s.M + 1;
+  std::vector<long long> lo(nl * per), hi(nl * per);
+  std::vector<int> cnt(nl), has(nl);
+  long long hz = 0;
+  cudaStream_t st = c.stream;
+  cudaMemcpyAsync(lo.data(), c.tl_glo, 8 * lo.size(), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(hi.data(), c.tl_ghi, 8 * hi.size(), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(cnt.data(), c.tl_gcnt, 4 * nl, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(has.data(), c.tl_ghas, 4 * nl, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&hz, c.tl_hz, 8, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return c.cuda_fail(e, "bubbles");
+  if (hz <= 0) {
+    c.set_error("horizon: must be positive");
+    return GPB_CONFIG_ERROR;
+  }
+  // expand to every timeline GPU in id order (extract_bubbles sorts by GPU):
+  // DCs in topology order; inside a DC ids go (cell, pipeline, stage).
+  const DevScen& sc = c.dev_scens_host[c.row_scen_host[row]];
+  const DevTopo& tp = c.dev_topos_host[sc.topo];
+  HostBlocks hb = host_decode(sc, tp, s.D);
+  int64_t k = 0;
+  for (int dc = 0; dc < tp.n_dc; ++dc) {
+    int b = -1;
+    for (int x = 0; x < hb.nb; ++x)
+      if (hb.dc[x] == dc) b = x;
+    if (b < 0) continue;
+    const int cnt_stages = hb.first[b + 1] - hb.first[b];
+    for (int cell = 0; cell < s.D; ++cell)
+      for (int pipe = 0; pipe < s.C; ++pipe)
+        for (int st2 = hb.first[b]; st2 < hb.first[b + 1]; ++st2) {
+          const int li = (s.Ce > 1 ? pipe : 0) * s.S + st2;
+          if (!has[li]) continue;  // no busy span: absent from busy_by_gpu
+          const int gpu = tp.dc_base[dc] +
+                          sc.tp * ((cell * s.C + pipe) * cnt_stages + (st2 - hb.first[b]));
+          for (int j = 0; j < cnt[li]; ++j, ++k) {
+            if (k < cap && out) {
+              out[k].gpu_id = gpu;
+              out[k].pad_ = 0;
+              out[k].start_ns = lo[li * per + j];
+              out[k].end_ns = hi[li * per + j];
+            }
+          }
+        }
+  }
+  if (n_out) *n_out = k;
+  return GPB_OK;
+}
+
+extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_rows_sel,
+                                 const gpb_request* reqs, int64_t n_req,
+                                 const gpb_prefill_model* pm, int64_t horizon_ns,
+                                 gpb_pack_summary* summaries, gpb_placement* placements) {
+  if (!ctx_) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  c.last_error.clear();
+  if (!c.loaded) {
+    c.set_error("no plan space loaded");
+    return GPB_CONFIG_ERROR;
+  }
+  if (!pm || n_rows_sel < 0 || n_req < 0 || (n_req > 0 && !reqs) || !summaries) {
+    c.set_error("null input");
+    return GPB_CONFIG_ERROR;
+  }
+  if (!(pm->saturation_ms > 0) || pm->max_tokens < 1 || pm->inference_layers < 1 ||
+      pm->inference_hidden < 1 || pm->bytes_per_element < 1 || pm->memory_budget_bytes < 1 ||
+      pm->boundary_latency_ms < 0 || pm->guard_ms < 0 || pm->inference_params_per_layer < 0) {
+    c.set_error("prefill: invalid prefill model");
+    return GPB_CONFIG_ERROR;
+  }
+  if (!(pm->stage_bw > 0)) {
+    c.set_error("bandwidth must be positive");
+    return GPB_ERROR;  // std::invalid_argument in transfer_time_ms
+  }
+  for (int64_t i = 0; i < n_req; ++i)
+    if (reqs[i].tokens < 1 || reqs[i].tokens > pm->max_tokens) {
+      c.set_error("request.tokens: must be in [1, %d]", pm->max_tokens);
+      return GPB_CONFIG_ERROR;
+    }
+  cudaSetDevice(c.device);
+  cudaEventRecord(c.ev0, c.stream);
+  std::vector<TlSlot> slots;
+  int rc = build_timelines(c, rows, n_rows_sel, horizon_ns, slots);
+  if (rc != GPB_OK) return rc;
+  // memory budget per stage (bubbletea.cpp:113-125)
+  const double ppl = pm->inference_params_per_layer > 0
+                         ? pm->inference_params_per_layer
+                         : 12.0 * (double)pm->inference_hidden * (double)pm->inference_hidden;
+  std::vector<long long> gpu_base(n_rows_sel + 1, 0);
+  long long max_nl = 0;
+  for (int i = 0; i < n_rows_sel; ++i) {
+    const TlSlot& s = slots[i];
+    const int worst = pm->inference_layers / s.D + (pm->inference_layers % s.D ? 1 : 0);
+    const long long mem = (long long)((double)worst * ppl * pm->bytes_per_element);
+    if (mem > pm->memory_budget_bytes) {
+      c.set_error("prefill.memory_budget_bytes: inference model needs %lld bytes per stage, over "
+                  "the budget of %lld", mem, (long long)pm->memory_budget_bytes);
+      return GPB_CONFIG_ERROR;
+    }
+    gpu_base[i + 1] = gpu_base[i] + (long long)s.D * s.C * s.S;
+    max_nl = std::max(max_nl, (long long)s.Ce * s.S * (2 * s.M + 1));
+  }
+  cudaStream_t st = c.stream;
+  gpb_request* dreq = (gpb_request*)c.dev_buf(c.b_pl, sizeof(gpb_request) * std::max<int64_t>(1, n_req));
+  gpb_pack_summary* dsum = (gpb_pack_summary*)c.dev_buf(c.b_sum, sizeof(gpb_pack_summary) * std::max(1, n_rows_sel) + 64);
+  const long long G = gpu_base[n_rows_sel];
+  long long* gpu_arr = (long long*)c.dev_buf(c.b_pack_scratch, 16 * (size_t)std::max(1LL, G) + 8 * (n_rows_sel + 1));
+  if (!dreq || !dsum || !gpu_arr) return c.cuda_fail(cudaErrorMemoryAllocation, "pack buffers");
+  long long* gpu_off = gpu_arr;
+  int* gpu_cnt = (int*)(gpu_off + std::max(1LL, G));
+  int* gpu_cap = gpu_cnt + std::max(1LL, G);
+  long long* dbase = (long long*)(gpu_cap + std::max(1LL, G));  // 16*G bytes in: aligned
+  int* overflow = (int*)(dsum + std::max(1, n_rows_sel));
+  cudaMemcpyAsync(dreq, reqs, sizeof(gpb_request) * n_req, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(dbase, gpu_base.data(), 8 * n_rows_sel, cudaMemcpyHostToDevice, st);
+  gpb_placement* dpl = nullptr;
+  if (placements) {
+    dpl = (gpb_placement*)c.dev_buf(c.b_placements, sizeof(gpb_placement) * (size_t)n_rows_sel * std::max<int64_t>(1, n_req));
+    if (!dpl) return c.cuda_fail(cudaErrorMemoryAllocation, "placements");
+  }
+  long long pool = std::max(4096LL, 4 * max_nl);
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    long long* pool_lo = (long long*)c.dev_buf(c.b_tl_scratch, 17 * (size_t)pool * std::max(1, n_rows_sel));
+    if (!pool_lo) return c.cuda_fail(cudaErrorMemoryAllocation, "pack pool");
+    PackArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.slots = (const TlSlot*)c.tl_slots_dev;
+    a.n_slots = n_rows_sel;
+    a.scens = (const DevScen*)c.b_scens.ptr;
+    a.topos = (const DevTopo*)c.b_topos.ptr;
+    a.row_scen = (const int32_t*)c.b_row_scen.ptr;
+    a.glo = c.tl_glo;
+    a.ghi = c.tl_ghi;
+    a.gflag = c.tl_gfl;
+    a.gcnt = c.tl_gcnt;
+    a.gsum = c.tl_gsum;
+    a.hz = c.tl_hz;
+    a.reqs = dreq;
+    a.n_req = n_req;
+    a.sat_ms = pm->saturation_ms;
+    a.stage_bw = pm->stage_bw;
+    a.lat_ms = pm->boundary_latency_ms;
+    a.max_tokens = pm->max_tokens;
+    a.inf_layers = pm->inference_layers;
+    a.bpe = pm->bytes_per_element;
+    a.inf_hidden = pm->inference_hidden;
+    a.guard_ns = host_ms_to_ns(pm->guard_ms);
+    a.pool_lo = pool_lo;
+    a.pool_hi = pool_lo + pool * n_rows_sel;
+    a.pool_fl = (unsigned char*)(a.pool_hi + pool * n_rows_sel);
+    a.pool_per_slot = pool;
+    a.gpu_off = gpu_off;
+    a.gpu_cnt = gpu_cnt;
+    a.gpu_cap = gpu_cap;
+    a.gpu_base = dbase;
+    a.sums = dsum;
+    a.pl = dpl;
+    a.overflow = overflow;
+    cudaMemsetAsync(overflow, 0, 4, st);
+    pack_kernel<<<(n_rows_sel + 3) / 4, 128, 0, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return c.cuda_fail(e, "pack launch");
+    int32_t ovf = 0;
+    cudaMemcpyAsync(&ovf, overflow, 4, cudaMemcpyDeviceToHost, st);
+    cudaEventRecord(c.ev3, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return c.cuda_fail(e, "pack");
+    if (!ovf) break;
+    if (attempt == 7) {
+      c.set_error("gap pool overflow");
+      return GPB_ERROR;
+    }
+    pool *= 4;
+    cudaEventRecord(c.ev0, st);
+  }
+  cudaEventElapsedTime(&c.pack_ms, c.ev0, c.ev3);
+  cudaMemcpyAsync(summaries, dsum, sizeof(gpb_pack_summary) * n_rows_sel, cudaMemcpyDeviceToHost, st);
+  if (placements)
+    cudaMemcpyAsync(placements, dpl, sizeof(gpb_placement) * (size_t)n_rows_sel * n_req,
+                    cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? GPB_OK : c.cuda_fail(e, "pack results");
+}

@@ -59,6 +59,12 @@ struct Ctx {
       b_sum, b_pack_scratch, b_pack_misc;
 
   std::vector<cudaEvent_t> bucket_ev;  // [buckets + 1]
+  Buf b_placements;
+  // last build_timelines() outputs (device pointers into the buffers above)
+  long long *tl_glo = nullptr, *tl_ghi = nullptr, *tl_gsum = nullptr, *tl_hz = nullptr;
+  unsigned char* tl_gfl = nullptr;
+  int *tl_gcnt = nullptr, *tl_ghas = nullptr;
+  void* tl_slots_dev = nullptr;
   bool timing_valid = false;
   int last_launches = 0;
   float pack_ms = 0.f;
@@ -66,7 +72,8 @@ struct Ctx {
   std::vector<Buf*> all_bufs() {
     return {&b_topos, &b_scens, &b_row_scen, &b_work, &b_rows, &b_results, &b_cursors,
             &b_best, &b_scratch, &b_cycles, &b_tl_rows, &b_tl_spans, &b_tl_nspan, &b_tl_scratch,
-            &b_gaps, &b_ngaps, &b_reqs, &b_pl, &b_sum, &b_pack_scratch, &b_pack_misc};
+            &b_gaps, &b_ngaps, &b_reqs, &b_pl, &b_sum, &b_pack_scratch, &b_pack_misc,
+            &b_placements};
   }
 
   void set_error(const char* fmt, ...);

@@ -26,6 +26,11 @@ struct EvalArgs {
   gpb_row* rows;              // output table
   int32_t* error_flag;
   long long* row_cycles;      // optional per-row clock64 cost (profiling)
+  // timeline variant: per-work-item offsets into forward-end / pair-start
+  // arrays laid out [pipeline][stage][microbatch]
+  long long* tl_fe;
+  long long* tl_ps;
+  const long long* tl_off;
   // flush: per-warp shared fd_last buffer length (max M of the bucket)
   int32_t smem_m;
   // atlas: per-warp shared slice and (when it does not fit) global garr
@@ -47,6 +52,8 @@ cudaError_t launch_flush(int B, bool gpipe, const EvalArgs& a, int grid, cudaStr
 cudaError_t launch_onef1b(int B, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_atlas(int B, const EvalArgs& a, int grid, int wpc, cudaStream_t st);
 cudaError_t launch_select(const SelectArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_timeline(int policy, int B, const EvalArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_atlas_timeline(int B, const EvalArgs& a, int grid, int wpc, cudaStream_t st);
 
 }  // namespace gpb
 

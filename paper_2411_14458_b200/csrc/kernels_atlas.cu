@@ -506,6 +506,56 @@ __global__ void __launch_bounds__(kEvalThreads) atlas_kernel(EvalArgs a) {
 }
 
 template <int B>
+__global__ void __launch_bounds__(kEvalThreads) atlas_timeline_kernel(EvalArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  const int gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
+  AtlasMem X;
+  X.carve(smem + (size_t)warp * a.lay.total, a.lay,
+          a.scratch ? a.scratch + (size_t)gwarp * a.scratch_per_warp : nullptr);
+  for (;;) {
+    const int wk = next_work(a.cursor);
+    if (wk >= a.n_work) break;
+    const int row = a.work[wk];
+    const long long t_start = clock64();
+    Geom g;
+    const DevScen* sc;
+    const DevTopo* tp;
+    if (!begin_row(a, row, g, sc, tp)) continue;
+    X.fe = a.tl_fe + a.tl_off[wk];
+    X.ps = a.tl_ps + a.tl_off[wk];
+    int err = 0;
+    const long long mk = atlas_row<B, true>(g, sc->mem_limit, X, err);
+    end_row(a, row, g, *sc, *tp, mk, err, t_start);
+    __syncwarp();
+  }
+}
+
+template <int B>
+static cudaError_t launch_atlas_tl_b(const EvalArgs& a, int grid, int wpc, cudaStream_t st) {
+  const size_t smem = (size_t)wpc * a.lay.total;
+  cudaError_t e = cudaFuncSetAttribute(atlas_timeline_kernel<B>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  atlas_timeline_kernel<B><<<grid, 32 * wpc, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_atlas_timeline(int B, const EvalArgs& a, int grid, int wpc, cudaStream_t st) {
+  switch (B) {
+    case 1: return launch_atlas_tl_b<1>(a, grid, wpc, st);
+    case 2: return launch_atlas_tl_b<2>(a, grid, wpc, st);
+    case 3: return launch_atlas_tl_b<3>(a, grid, wpc, st);
+    case 4: return launch_atlas_tl_b<4>(a, grid, wpc, st);
+    case 5: return launch_atlas_tl_b<5>(a, grid, wpc, st);
+    case 6: return launch_atlas_tl_b<6>(a, grid, wpc, st);
+    case 7: return launch_atlas_tl_b<7>(a, grid, wpc, st);
+    case 8: return launch_atlas_tl_b<8>(a, grid, wpc, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int B>
 static cudaError_t launch_atlas_b(const EvalArgs& a, int grid, int wpc, cudaStream_t st) {
   const size_t smem = (size_t)wpc * a.lay.total;
   cudaError_t e = cudaFuncSetAttribute(atlas_kernel<B>,

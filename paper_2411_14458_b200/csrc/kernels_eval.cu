@@ -26,8 +26,9 @@ namespace gpb {
 
 // ---------------------------------------------------------------- flush
 
-template <int B, bool GPIPE>
-__device__ long long flush_row(const Geom& g, long long* fdl) {
+template <int B, bool GPIPE, bool TL = false>
+__device__ long long flush_row(const Geom& g, long long* fdl, long long* tfe = nullptr,
+                               long long* tps = nullptr) {
   const int lane = threadIdx.x & 31;
   const int S = g.S, M = g.M;
   const int K = (S - 1) / B;  // highest lane that owns a stage
@@ -50,6 +51,7 @@ __device__ long long flush_row(const Geom& g, long long* fdl) {
           const long long e = imax(a, gf[j]) + g.fwd;
           gf[j] = e;
           if (s == S - 1) fdl[m] = e;
+          if (TL) tfe[(size_t)s * M + m] = e;
           if ((L.wanf >> j) & 1u) {
             const long long occ = imax(e, lf[j]) + L.serf[j];
             lf[j] = occ;
@@ -79,6 +81,7 @@ __device__ long long flush_row(const Geom& g, long long* fdl) {
           ready = imax(ready, beta);
           const long long z = imax(ready, gf[j]) + g.dur;
           gf[j] = z;
+          if (TL) tps[(size_t)s * M + m] = z - g.dur;
           if (s > 0) {
             if ((L.wanb >> j) & 1u) {
               const long long occ = imax(z, lb[j]) + L.serb[j];
@@ -137,8 +140,9 @@ __device__ __forceinline__ void onef1b_item(int pc, int w, int M, bool& fwd, int
   }
 }
 
-template <int B>
-__device__ long long onef1b_row(const Geom& g, int& err) {
+template <int B, bool TL = false>
+__device__ long long onef1b_row(const Geom& g, int& err, long long* tfe = nullptr,
+                                long long* tps = nullptr) {
   const int lane = threadIdx.x & 31;
   const int S = g.S, M = g.M;
   StageLinks<B> L;
@@ -190,6 +194,7 @@ __device__ long long onef1b_row(const Geom& g, int& err) {
         const long long e = imax(arr, gf[j]) + g.fwd;
         gf[j] = e;
         fdo[j] = e;
+        if (TL) tfe[(size_t)s * M + m] = e;
         if (s + 1 < S) {
           if ((L.wanf >> j) & 1u) {
             const long long occ = imax(e, lf[j]) + L.serf[j];
@@ -213,6 +218,7 @@ __device__ long long onef1b_row(const Geom& g, int& err) {
         }
         const long long z = imax(ready, gf[j]) + g.dur;
         gf[j] = z;
+        if (TL) tps[(size_t)s * M + m] = z - g.dur;
         if (s > 0) {
           if ((L.wanb >> j) & 1u) {
             const long long occ = imax(z, lb[j]) + L.serb[j];
@@ -250,6 +256,69 @@ __global__ void __launch_bounds__(kEvalThreads) onef1b_kernel(EvalArgs a) {
     end_row(a, row, g, *sc, *tp, mk, err, t_start);
     __syncwarp();
   }
+}
+
+// ------------------------------------------------------------- timeline
+
+// Timeline variants for gpipe/1f1b/varuna: every pipeline of a cell is
+// identical, so pipeline 0 stands for all of them.
+template <int B, int POLICY>
+__global__ void __launch_bounds__(kEvalThreads) timeline_kernel(EvalArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  long long* fdl = reinterpret_cast<long long*>(smem) + (size_t)warp * a.smem_m;
+  for (;;) {
+    const int w = next_work(a.cursor);
+    if (w >= a.n_work) break;
+    const int row = a.work[w];
+    const long long t_start = clock64();
+    Geom g;
+    const DevScen* sc;
+    const DevTopo* tp;
+    if (!begin_row(a, row, g, sc, tp)) continue;
+    long long* tfe = a.tl_fe + a.tl_off[w];
+    long long* tps = a.tl_ps + a.tl_off[w];
+    int err = 0;
+    long long mk;
+    if (POLICY == GPB_1F1B) {
+      mk = onef1b_row<B, true>(g, err, tfe, tps);
+    } else {
+      mk = flush_row<B, POLICY == GPB_GPIPE, true>(g, fdl, tfe, tps);
+    }
+    end_row(a, row, g, *sc, *tp, mk, err, t_start);
+    __syncwarp();
+  }
+}
+
+template <int B>
+static cudaError_t launch_timeline_b(int policy, const EvalArgs& a, int grid, cudaStream_t st) {
+  const size_t smem = (size_t)(kEvalThreads / 32) * a.smem_m * sizeof(long long);
+  if (policy == GPB_GPIPE) {
+    cudaFuncSetAttribute(timeline_kernel<B, GPB_GPIPE>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    timeline_kernel<B, GPB_GPIPE><<<grid, kEvalThreads, smem, st>>>(a);
+  } else if (policy == GPB_VARUNA) {
+    cudaFuncSetAttribute(timeline_kernel<B, GPB_VARUNA>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    timeline_kernel<B, GPB_VARUNA><<<grid, kEvalThreads, smem, st>>>(a);
+  } else {
+    timeline_kernel<B, GPB_1F1B><<<grid, kEvalThreads, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_timeline(int policy, int B, const EvalArgs& a, int grid, cudaStream_t st) {
+  switch (B) {
+    case 1: return launch_timeline_b<1>(policy, a, grid, st);
+    case 2: return launch_timeline_b<2>(policy, a, grid, st);
+    case 3: return launch_timeline_b<3>(policy, a, grid, st);
+    case 4: return launch_timeline_b<4>(policy, a, grid, st);
+    case 5: return launch_timeline_b<5>(policy, a, grid, st);
+    case 6: return launch_timeline_b<6>(policy, a, grid, st);
+    case 7: return launch_timeline_b<7>(policy, a, grid, st);
+    case 8: return launch_timeline_b<8>(policy, a, grid, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 // -------------------------------------------------------------- select
