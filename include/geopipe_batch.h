@@ -221,6 +221,14 @@ int gpb_copy_best(gpb_ctx* ctx, void* dst);
 int gpb_bubbles(gpb_ctx* ctx, int64_t row, int64_t horizon_ns,
                 gpb_bubble* out, int64_t cap, int64_t* n_out);
 
+/* Raw iteration timeline of one row's cell 0 (all D cells are identical):
+ * forward end times and pair (recompute+backward) start times, laid out
+ * [pipeline][stage][microbatch] with Ce = C pipelines for atlas and 1
+ * otherwise (spatial policies schedule every pipeline identically).
+ * dims receives {Ce, S, M, D}; arrays are written when cap >= Ce*S*M. */
+int gpb_timeline_arrays(gpb_ctx* ctx, int64_t row, int64_t* fe, int64_t* ps,
+                        int64_t cap, int32_t* dims, int64_t* makespan);
+
 /* BubbleTea: pack one request trace (sorted by arrival, FCFS) into the
  * bubbles of each listed row, independently per row (schedule_prefills,
  * bubbletea.cpp:132-222). horizon_ns <= 0 => each row's makespan.
@@ -229,6 +237,11 @@ int gpb_pack_prefills(gpb_ctx* ctx, const int64_t* rows, int32_t n_rows_sel,
                       const gpb_request* reqs, int64_t n_req,
                       const gpb_prefill_model* pm, int64_t horizon_ns,
                       gpb_pack_summary* summaries, gpb_placement* placements);
+
+/* Include each stage's all-reduce tail (append_allreduce,
+ * scheduler.cpp:613-650; the simulate.allreduce option) in the timelines
+ * behind gpb_bubbles and gpb_pack_prefills. Default off. */
+int gpb_set_allreduce_tail(gpb_ctx* ctx, int32_t enable);
 
 /* Deterministic request sources on the host (bubbletea.cpp:240-284). */
 int gpb_synthetic_requests(int32_t count, uint32_t seed, double horizon_ms,

@@ -38,8 +38,40 @@ struct TlSlot {
   long long lst_off;  // into per-list arrays ([Ce][S])
   long long horizon;  // <= 0: makespan of the row
   long long fwd, dur;
+  long long ar_off;   // >= 0: all-reduce tail durations at ar_dur[ar_off + s]
   int S, M, Ce, C, D, policy;
 };
+
+// Horizon per slot: the given one, else the makespan of the timeline incl.
+// the optional all-reduce tail (append_allreduce, scheduler.cpp:613-650:
+// each stage's all-reduce starts at the stage's last backward end over all
+// replicas).
+__global__ void horizon_kernel(const TlSlot* slots, int n_slots, const gpb_row* tl_rows,
+                               const long long* ps, const long long* ar_dur,
+                               long long* ar_start, long long* hz_out) {
+  const int si = blockIdx.x;
+  if (si >= n_slots) return;
+  const TlSlot& sl = slots[si];
+  long long mk = tl_rows[sl.row].makespan_ns;
+  if (sl.ar_off >= 0) {
+    for (int s = threadIdx.x; s < sl.S; s += blockDim.x) {
+      long long last = 0;
+      for (int p = 0; p < sl.Ce; ++p)
+        for (int m = 0; m < sl.M; ++m)
+          last = imax(last, ps[sl.tl_off + ((size_t)p * sl.S + s) * sl.M + m] + sl.dur);
+      ar_start[sl.ar_off + s] = last;
+      atomicMax((unsigned long long*)&hz_out[si], (unsigned long long)(last + ar_dur[sl.ar_off + s]));
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (sl.horizon > 0) {
+      hz_out[si] = sl.horizon;
+    } else {
+      hz_out[si] = imax(mk, sl.ar_off >= 0 ? hz_out[si] : 0);
+    }
+  }
+}
 
 __device__ __forceinline__ unsigned long long fnv_mix(unsigned long long h, unsigned long long v) {
   for (int i = 0; i < 8; ++i) {
@@ -49,10 +81,11 @@ __device__ __forceinline__ unsigned long long fnv_mix(unsigned long long h, unsi
   return h;
 }
 
-__global__ void gap_kernel(const TlSlot* slots, int n_slots, const gpb_row* tl_rows,
-                           const long long* fe, const long long* ps, long long* glo,
-                           long long* ghi, unsigned char* gflag, int* gcnt,
-                           long long* gsum, int* ghas, long long* hz_out) {
+__global__ void gap_kernel(const TlSlot* slots, int n_slots, const long long* fe,
+                           const long long* ps, const long long* ar_dur,
+                           const long long* ar_start, long long* glo, long long* ghi,
+                           unsigned char* gflag, int* gcnt, long long* gsum, int* ghas,
+                           const long long* hz) {
   // grid.y = slot, threads over its (pipeline, stage) lists
   const int si = blockIdx.y;
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -61,8 +94,11 @@ __global__ void gap_kernel(const TlSlot* slots, int n_slots, const gpb_row* tl_r
   if (gid >= (long long)sl.Ce * sl.S) return;
   const int M = sl.M;
   const int li = (int)gid;  // = p * S + s
-  const long long H = sl.horizon > 0 ? sl.horizon : tl_rows[sl.row].makespan_ns;
-  if (li == 0) hz_out[si] = H;
+  const long long H = hz[si];
+  const int s_idx = li % sl.S;
+  const bool ar = sl.ar_off >= 0;
+  const long long ar_lo = ar ? ar_start[sl.ar_off + s_idx] : 0;
+  const long long ar_hi = ar ? ar_lo + ar_dur[sl.ar_off + s_idx] : 0;
   const long long* F = fe + sl.tl_off + (size_t)li * M;
   const long long* P = ps + sl.tl_off + (size_t)li * M;
   long long* lo_out = glo + sl.gap_off + (size_t)li * (2 * M + 1);
@@ -71,12 +107,17 @@ __global__ void gap_kernel(const TlSlot* slots, int n_slots, const gpb_row* tl_r
   const bool rev = sl.policy == GPB_GPIPE;  // gpipe drains in reverse order
   int i_f = 0, i_p = 0, n = 0, has = 0;
   long long cursor = 0, sum = 0;
-  while (i_f < M || i_p < M) {
+  bool ar_done = !ar;
+  while (i_f < M || i_p < M || !ar_done) {
     long long fs = kInf64, pst = kInf64;
     if (i_f < M) fs = F[i_f] - sl.fwd;
     if (i_p < M) pst = P[rev ? M - 1 - i_p : i_p];
     long long lo, hi;
-    if (fs <= pst) {
+    if (i_f >= M && i_p >= M) {  // the all-reduce tail comes last on its GPU
+      lo = ar_lo;
+      hi = ar_hi;
+      ar_done = true;
+    } else if (fs <= pst) {
       lo = fs;
       hi = fs + sl.fwd;
       ++i_f;
@@ -483,10 +524,11 @@ long long host_ms_to_ns(double ms) { return std::llround(ms * 1e6); }
 
 // Runs the timeline kernels for `rows` and the gap kernel; fills slots.
 int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
-                    std::vector<TlSlot>& slots) {
+                    std::vector<TlSlot>& slots, bool with_allreduce = false) {
   cudaStream_t st = c.stream;
   slots.resize(n);
   long long tl = 0, gp = 0, ls = 0;
+  std::vector<long long> ar_host;
   for (int i = 0; i < n; ++i) {
     if (rows[i] < 0 || rows[i] >= c.n_rows) {
       c.set_error("row index out of range");
@@ -515,6 +557,20 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
     s.tl_off = tl;
     s.gap_off = gp;
     s.lst_off = ls;
+    s.ar_off = -1;
+    if (with_allreduce) {
+      // allreduce_time_ms per stage (comm_model.cpp:38-41) -> ms_to_ns
+      s.ar_off = (long long)ar_host.size();
+      const int N = d * sc.C;
+      for (int st2 = 0; st2 < sc.S; ++st2) {
+        int b = 0;
+        while (b + 1 < hb.nb && st2 >= hb.first[b + 1]) ++b;
+        const int begin = st2 * sc.lpp, end = std::min(begin + sc.lpp, sc.L);
+        const double params = sc.ppl * std::max(0, end - begin);
+        const double ms = N <= 1 ? 0.0 : 4.0 * params * (N - 1) / (N * tp.intra_bw[hb.dc[b]]);
+        ar_host.push_back(host_ms_to_ns(ms));
+      }
+    }
     tl += (long long)s.Ce * s.S * s.M;
     gp += (long long)s.Ce * s.S * (2 * s.M + 1);
     ls += (long long)s.Ce * s.S;
@@ -611,10 +667,17 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
     }
     if (e != cudaSuccess) return c.cuda_fail(e, "timeline launch");
   }
+  long long* ar_dev = (long long*)c.dev_buf(c.b_ar, 16 * std::max<size_t>(1, ar_host.size()));
+  if (!ar_dev) return c.cuda_fail(cudaErrorMemoryAllocation, "allreduce buffers");
+  long long* ar_start = ar_dev + std::max<size_t>(1, ar_host.size());
+  if (!ar_host.empty())
+    cudaMemcpyAsync(ar_dev, ar_host.data(), 8 * ar_host.size(), cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(hz, 0, 8 * (size_t)n, st);
+  horizon_kernel<<<n, 128, 0, st>>>(dslots, n, tl_rows, ps, ar_dev, ar_start, hz);
   long long max_lists = 1;
   for (const TlSlot& s : slots) max_lists = std::max(max_lists, (long long)s.Ce * s.S);
   gap_kernel<<<dim3((unsigned)((max_lists + 127) / 128), (unsigned)n), 128, 0, st>>>(
-      dslots, n, tl_rows, fe, ps, glo, ghi, gfl, gcnt, gsum, ghas, hz);
+      dslots, n, fe, ps, ar_dev, ar_start, glo, ghi, gfl, gcnt, gsum, ghas, hz);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return c.cuda_fail(e, "gap kernel");
   int32_t flag = 0;
@@ -648,7 +711,7 @@ extern "C" int gpb_bubbles(gpb_ctx* ctx_, int64_t row, int64_t horizon_ns, gpb_b
   }
   cudaSetDevice(c.device);
   std::vector<TlSlot> slots;
-  int rc = build_timelines(c, &row, 1, horizon_ns, slots);
+  int rc = build_timelines(c, &row, 1, horizon_ns, slots, c.pack_allreduce);
   if (rc != GPB_OK) return rc;
   const TlSlot& s = slots[0];
   const size_t nl = (size_t)s.Ce * s.S, per = 2 * (size_t)s.M + 1;
@@ -733,7 +796,7 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
   cudaSetDevice(c.device);
   cudaEventRecord(c.ev0, c.stream);
   std::vector<TlSlot> slots;
-  int rc = build_timelines(c, rows, n_rows_sel, horizon_ns, slots);
+  int rc = build_timelines(c, rows, n_rows_sel, horizon_ns, slots, c.pack_allreduce);
   if (rc != GPB_OK) return rc;
   // memory budget per stage (bubbletea.cpp:113-125)
   const double ppl = pm->inference_params_per_layer > 0
@@ -832,4 +895,45 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
                     cudaMemcpyDeviceToHost, st);
   cudaError_t e = cudaStreamSynchronize(st);
   return e == cudaSuccess ? GPB_OK : c.cuda_fail(e, "pack results");
+}
+
+// Raw iteration timeline of one row (cell 0): forward ends and pair starts
+// laid out [pipeline][stage][microbatch] (Ce = C for atlas, else 1).
+extern "C" int gpb_timeline_arrays(gpb_ctx* ctx_, int64_t row, int64_t* fe, int64_t* ps,
+                                   int64_t cap, int32_t* dims, int64_t* makespan) {
+  if (!ctx_ || !dims) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  c.last_error.clear();
+  if (!c.loaded) {
+    c.set_error("no plan space loaded");
+    return GPB_CONFIG_ERROR;
+  }
+  cudaSetDevice(c.device);
+  std::vector<TlSlot> slots;
+  int rc = build_timelines(c, &row, 1, 0, slots);
+  if (rc != GPB_OK) return rc;
+  const TlSlot& s = slots[0];
+  const long long n = (long long)s.Ce * s.S * s.M;
+  dims[0] = s.Ce;
+  dims[1] = s.S;
+  dims[2] = s.M;
+  dims[3] = s.D;
+  if (fe && ps && cap >= n) {
+    long long* dfe = (long long*)c.b_tl_spans.ptr;
+    long long* dps = dfe + std::max(1LL, n);
+    cudaMemcpyAsync(fe, dfe, 8 * n, cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(ps, dps, 8 * n, cudaMemcpyDeviceToHost, c.stream);
+  }
+  gpb_row r;
+  cudaMemcpyAsync(&r, (gpb_row*)c.b_tl_rows.ptr + row, sizeof r, cudaMemcpyDeviceToHost, c.stream);
+  cudaError_t e = cudaStreamSynchronize(c.stream);
+  if (e != cudaSuccess) return c.cuda_fail(e, "timeline");
+  if (makespan) *makespan = r.makespan_ns;
+  return GPB_OK;
+}
+
+extern "C" int gpb_set_allreduce_tail(gpb_ctx* ctx_, int32_t enable) {
+  if (!ctx_) return GPB_ERROR;
+  reinterpret_cast<Ctx*>(ctx_)->pack_allreduce = enable != 0;
+  return GPB_OK;
 }

@@ -59,7 +59,8 @@ struct Ctx {
       b_sum, b_pack_scratch, b_pack_misc;
 
   std::vector<cudaEvent_t> bucket_ev;  // [buckets + 1]
-  Buf b_placements;
+  Buf b_placements, b_ar;
+  bool pack_allreduce = false;  // include the all-reduce tail in timelines
   // last build_timelines() outputs (device pointers into the buffers above)
   long long *tl_glo = nullptr, *tl_ghi = nullptr, *tl_gsum = nullptr, *tl_hz = nullptr;
   unsigned char* tl_gfl = nullptr;
@@ -73,7 +74,7 @@ struct Ctx {
     return {&b_topos, &b_scens, &b_row_scen, &b_work, &b_rows, &b_results, &b_cursors,
             &b_best, &b_scratch, &b_cycles, &b_tl_rows, &b_tl_spans, &b_tl_nspan, &b_tl_scratch,
             &b_gaps, &b_ngaps, &b_reqs, &b_pl, &b_sum, &b_pack_scratch, &b_pack_misc,
-            &b_placements};
+            &b_placements, &b_ar};
   }
 
   void set_error(const char* fmt, ...);

@@ -77,6 +77,9 @@ def load_library(path: str = LIB_PATH):
         "gpb_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
         "gpb_copy_best": (C.c_int, [C.c_void_p, C.c_void_p]),
         "gpb_set_profile": (C.c_int, [C.c_void_p, C.c_int32]),
+        "gpb_set_allreduce_tail": (C.c_int, [C.c_void_p, C.c_int32]),
+        "gpb_timeline_arrays": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_int64), P(C.c_int64),
+                                          C.c_int64, P(C.c_int32), P(C.c_int64)]),
         "gpb_fetch_row_cycles": (C.c_int, [C.c_void_p, P(C.c_int64), C.c_int64]),
     }
     for name, (res, args) in sig.items():
@@ -92,7 +95,8 @@ def exported_symbols():
             "gpb_load", "gpb_evaluate", "gpb_fetch_rows", "gpb_fetch_scenarios",
             "gpb_fetch_best", "gpb_device_best", "gpb_bubbles", "gpb_pack_prefills",
             "gpb_synthetic_requests", "gpb_get_timing", "gpb_microbench", "gpb_set_stream",
-            "gpb_copy_best", "gpb_set_profile", "gpb_fetch_row_cycles"]
+            "gpb_copy_best", "gpb_set_profile", "gpb_fetch_row_cycles",
+            "gpb_set_allreduce_tail", "gpb_timeline_arrays"]
 
 
 @dataclass

@@ -1,0 +1,128 @@
+"""GPU: the drop-in session ABI (include/geopipe.h, 17 gp_* functions)
+against the reference's own libgeopipe (compiled, unmodified, in
+oracle/_ref): same return codes and byte-identical artifacts
+(selection.csv, whatif.csv, metrics.csv, schedule.csv, trace.json,
+placements.csv, bubbletea_metrics.csv) and selection table."""
+import ctypes as C
+import glob
+import os
+
+import pytest
+
+from paper_2411_14458_b200 import planner as pl
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+CONFIGS = sorted(glob.glob(os.path.join(HERE, "golden", "configs", "*.json")))
+REF_SO = os.path.join(os.path.dirname(HERE), "oracle", "_ref", "libgeopipe_ref.so")
+
+
+class Session:
+    def __init__(self, path):
+        self.lib = C.CDLL(path)
+        L = self.lib
+        L.gp_session_create.restype = C.c_void_p
+        L.gp_session_destroy.argtypes = [C.c_void_p]
+        L.gp_last_error.restype = C.c_char_p
+        L.gp_last_error.argtypes = [C.c_void_p]
+        L.gp_selection_table.restype = C.c_char_p
+        L.gp_selection_table.argtypes = [C.c_void_p]
+        for n in ("gp_load_config_file", "gp_load_config_text", "gp_set_policy", "gp_run_simulate",
+                  "gp_run_trace", "gp_run_select_dc", "gp_run_whatif", "gp_run_bubbletea"):
+            getattr(L, n).argtypes = [C.c_void_p, C.c_char_p]
+        L.gp_set_seed.argtypes = [C.c_void_p, C.c_uint]
+        for n in ("gp_set_multi_conn", "gp_set_recompute", "gp_set_mem_limit"):
+            getattr(L, n).argtypes = [C.c_void_p, C.c_int]
+        L.gp_set_horizon_ms.argtypes = [C.c_void_p, C.c_double]
+        self.s = L.gp_session_create()
+
+    def __getattr__(self, name):
+        fn = getattr(self.lib, "gp_" + name)
+        return lambda *a: fn(self.s, *a)
+
+    def close(self):
+        self.lib.gp_session_destroy(self.s)
+
+
+@pytest.fixture(scope="module")
+def libs():
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built")
+    return REF_SO, pl.LIB_PATH
+
+
+def _run(path, cfg, cmd, out, overrides=()):
+    s = Session(path)
+    try:
+        rc = s.load_config_file(cfg.encode()) if cfg else 0
+        for name, val in overrides:
+            assert getattr(s, "set_" + name)(val) == 0
+        rc = getattr(s, "run_" + cmd)(out.encode())
+        table = s.selection_table().decode()
+        return rc, table, s.last_error().decode()
+    finally:
+        s.close()
+
+
+def _files(d):
+    return {os.path.basename(p): open(p, "rb").read() for p in sorted(glob.glob(os.path.join(d, "*")))}
+
+
+CASES = []
+for cfg in CONFIGS:
+    name = os.path.basename(cfg)
+    if "whatif" in name:
+        CASES += [(cfg, "whatif", ()), (cfg, "select_dc", ())]
+    elif "select" in name:
+        CASES += [(cfg, "select_dc", ()), (cfg, "select_dc", (("policy", b"varuna"),))]
+    elif "bubbletea" in name or "config1" in name:
+        CASES += [(cfg, "bubbletea", ()), (cfg, "simulate", ())]
+    else:
+        CASES += [(cfg, "simulate", ()), (cfg, "trace", ()), (cfg, "select_dc", ()),
+                  (cfg, "bubbletea", (("horizon_ms", 30.0),))]
+CASES += [(CONFIGS[0], "simulate", (("policy", b"gpipe"), ("recompute", 0))),
+          (CONFIGS[0], "simulate", (("mem_limit", 1),))]
+
+
+@pytest.mark.parametrize("cfg,cmd,ov", CASES,
+                         ids=[f"{os.path.basename(c)}-{m}-{len(o)}" for c, m, o in CASES])
+def test_artifacts_byte_identical(libs, tmp_path, cfg, cmd, ov):
+    ref_so, ours = libs
+    a, b = tmp_path / "ref", tmp_path / "ours"
+    ra = _run(ref_so, cfg, cmd, str(a), ov)
+    rb = _run(ours, cfg, cmd, str(b), ov)
+    assert ra[0] == rb[0], (ra, rb)
+    assert ra[1] == rb[1]
+    fa, fb = _files(a), _files(b)
+    assert fa.keys() == fb.keys()
+    for k in fa:
+        assert fa[k] == fb[k], k
+
+
+def test_error_codes_match(libs, tmp_path):
+    ref_so, ours = libs
+    cases = [
+        (None, "select_dc", ()),                      # no config loaded -> 2
+        (CONFIGS[0], "simulate", (("policy", b"pipedream"),)),  # deferred validation -> 2
+        (CONFIGS[0], "simulate", (("mem_limit", 0),)),
+        (CONFIGS[0], "simulate", (("horizon_ms", -1.0),)),
+    ]
+    for cfg, cmd, ov in cases:
+        ra = _run(ref_so, cfg, cmd, str(tmp_path / "a"), ov)
+        rb = _run(ours, cfg, cmd, str(tmp_path / "b"), ov)
+        assert ra[0] == rb[0], (cfg, cmd, ov, ra, rb)
+    # malformed JSON / infeasible plan via text configs
+    for text, want in ((b"{not json", 2), (b'{"datacenters": []}', 2)):
+        for so in (ref_so, ours):
+            s = Session(so)
+            assert s.load_config_text(text) == 0
+            assert s.run_select_dc(str(tmp_path / "c").encode()) == want
+            s.close()
+    unit12 = os.path.join(HERE, "golden", "configs", "unit12.json")
+    bad = open(unit12).read().replace('"dp_cells": 1', '"dp_cells": 50')
+    assert bad != open(unit12).read()
+    for so in (ref_so, ours):
+        s = Session(so)
+        s.load_config_text(bad.encode())
+        assert s.run_simulate(str(tmp_path / "d").encode()) == 3
+        s.close()
