@@ -230,6 +230,7 @@ def impl_ours(args):
     planner.set_stream(stream.cuda_stream)
     n_rows = planner.load(tarr, sarr)
     l2_flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    from paper_2411_14458_b200 import distributed as pdist
     best_t = torch.zeros(2, dtype=torch.int64, device="cuda")   # raw gpb_best
     gathered = torch.zeros(2 * world, dtype=torch.int64, device="cuda")
 
@@ -237,7 +238,7 @@ def impl_ours(args):
         if world > 1:
             # 16-byte per-GPU winner, D2D on the stream, then one NCCL all-gather
             planner.copy_best(best_t.data_ptr())
-            dist.all_gather_into_tensor(gathered, best_t)
+            pdist.all_gather_best(best_t, world, gathered)
 
     # warm-up
     for _ in range(args.warmup):
@@ -306,6 +307,11 @@ def impl_ours(args):
     rows1 = planner.rows()
     assert all(bytes(a) == bytes(b) for a, b in zip(rows0, rows1)), "non-deterministic rows"
 
+    global_winner = None
+    if world > 1:
+        recs = [pdist.decode_best(gathered[2 * r: 2 * r + 2].cpu()) for r in range(world)]
+        global_winner = pdist.reduce_best(recs)
+
     # roofline of the dominant kernel family
     ops = algorithmic_ops(scens, rows1)
     dom = max(range(4), key=lambda i: policy_ms[i])
@@ -329,6 +335,8 @@ def impl_ours(args):
                     "h2d_bytes_per_step": int(tinfo.h2d_bytes),
                     "d2h_bytes_per_step": int(tinfo.d2h_bytes // e2e_steps)},
             "gpu_launches": launches,
+            "global_best": ({"rank": global_winner[0], "throughput": global_winner[1],
+                             "row": global_winner[2]} if global_winner else None),
             "device_ms": {"evaluate": eval_ms / args.steps,
                           "per_policy": {abi.POLICY_NAMES[i]: policy_ms[i] / args.steps
                                          for i in range(4)}},
