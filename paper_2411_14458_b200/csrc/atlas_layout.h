@@ -24,8 +24,8 @@ struct AtlasLayout {
     const size_t CS = (size_t)C * S;
     cap = C * M;
     size_t o = 0;
-    off_wa = o;        o = al(o + 8 * 8);
-    off_wg = o;        o = al(o + 8 * 8);
+    off_wa = o;        o = al(o + 16 * 8);          // a_w [0,8) | ser_w [8,16)
+    off_wg = o;        o = al(o + 16 * 8);          // G_w [0,8) | lat_w [8,16)
     off_wbs = o;       o = al(o + (size_t)S * 4);   // WAN boundary before stage s
     off_gf = o;        o = al(o + CS * 8);
     off_cand = o;      o = al(o + CS * 8);

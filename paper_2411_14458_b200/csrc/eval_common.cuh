@@ -14,6 +14,9 @@ __device__ __forceinline__ long long shfl_up64(long long v, int d) {
 __device__ __forceinline__ long long shfl_down64(long long v, int d) {
   return __shfl_down_sync(kFull, v, d);
 }
+__device__ __forceinline__ long long shfl_idx64(long long v, int src) {
+  return __shfl_sync(kFull, v, src);
+}
 __device__ __forceinline__ long long warp_max64(long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = imax(v, __shfl_xor_sync(kFull, v, o));

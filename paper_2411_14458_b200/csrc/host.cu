@@ -105,6 +105,9 @@ Ctx::~Ctx() {
   if (ev2) cudaEventDestroy(ev2);
   if (ev3) cudaEventDestroy(ev3);
   for (cudaEvent_t e : bucket_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : bucket_ev_end) cudaEventDestroy(e);
+  for (cudaEvent_t e : side_done) cudaEventDestroy(e);
+  for (cudaStream_t s2 : side) cudaStreamDestroy(s2);
   if (own_stream) cudaStreamDestroy(own_stream);
 }
 
@@ -155,6 +158,8 @@ static void validate_scenario(const gpb_scenario& s, int idx, int n_topo,
   if (s.num_layers < 1) throw ConfigErr{"model.num_layers: must be >= 1"};
   if (s.layers_per_partition < 1) throw ConfigErr{"model.layers_per_partition: must be >= 1"};
   if (s.num_microbatches < 1) throw ConfigErr{"model.num_microbatches: must be >= 1"};
+  if (s.num_microbatches > 65535)
+    throw ConfigErr{P + ": more than 65535 microbatches is outside the kernel envelope"};
   if (s.bytes_per_element < 1 || s.hidden < 1 || s.seq_len < 1 || s.microbatch < 1)
     throw ConfigErr{"model: dimensions must be >= 1"};
   if (s.params_per_layer < 0) throw ConfigErr{"model.params_per_layer: must be >= 0"};
@@ -323,8 +328,17 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   // Buckets: (policy, B = ceil(S/32)); within a bucket scenarios are dealt
   // in decreasing estimated cost so the persistent warps finish together.
   c.buckets.clear();
-  std::map<std::pair<int, int>, std::vector<int>> by_key;
-  for (int i = 0; i < n_scen; ++i) by_key[{ds[i].policy, (ds[i].S + 31) / 32}].push_back(i);
+  // ATLAS rows are further split by the size class of their shared-memory
+  // slice (log2 of C*S*M) so small rows are not sized for the largest one.
+  std::map<std::tuple<int, int, int>, std::vector<int>> by_key;
+  for (int i = 0; i < n_scen; ++i) {
+    int cls = 0;
+    if (ds[i].policy == GPB_ATLAS) {
+      const long long csm = (long long)ds[i].C * ds[i].S * ds[i].M;
+      while ((1LL << cls) < csm) ++cls;
+    }
+    by_key[{ds[i].policy, (ds[i].S + 31) / 32, cls}].push_back(i);
+  }
   std::vector<int32_t> work;
   work.reserve(n_rows);
   for (auto& [key, list] : by_key) {
@@ -335,8 +349,8 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
     };
     std::stable_sort(list.begin(), list.end(), [&](int a, int b) { return cost(a) > cost(b); });
     Bucket b;
-    b.policy = key.first;
-    b.B = key.second;
+    b.policy = std::get<0>(key);
+    b.B = std::get<1>(key);
     b.offset = (int32_t)work.size();
     for (int i : list) {
       for (int k = 0; k < ds[i].n_rows; ++k) work.push_back((int32_t)(ds[i].first_row + k));
@@ -349,8 +363,12 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
       b.max_nw = std::max(b.max_nw, ds[i].n_order - 1);
     }
     b.count = (int32_t)work.size() - b.offset;
+    b.cost = cost(list.front());
     c.buckets.push_back(b);
   }
+  // longest rows first: their buckets are launched first on the side streams
+  std::stable_sort(c.buckets.begin(), c.buckets.end(),
+                   [](const Bucket& x, const Bucket& y) { return x.cost > y.cost; });
 
   // Upload (one H2D per table).
   cudaStream_t st = c.stream;
@@ -407,10 +425,33 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     if (cudaEventCreate(&e) != cudaSuccess) return c.cuda_fail(cudaGetLastError(), "event");
     c.bucket_ev.push_back(e);
   }
+  // buckets run concurrently on side streams forked from the launch stream
+  while (c.side.size() < kSideStreams) {
+    cudaStream_t s2;
+    cudaEvent_t e2;
+    if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e2, cudaEventDisableTiming) != cudaSuccess)
+      return c.cuda_fail(cudaGetLastError(), "side streams");
+    c.side.push_back(s2);
+    c.side_done.push_back(e2);
+  }
+  while (c.bucket_ev_end.size() < c.buckets.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return c.cuda_fail(cudaGetLastError(), "event");
+    c.bucket_ev_end.push_back(e);
+  }
+  cudaEventRecord(c.bucket_ev[c.buckets.size()], st);  // fork point
+  for (size_t k = 0; k < c.side.size(); ++k) cudaStreamWaitEvent(c.side[k], c.bucket_ev[c.buckets.size()], 0);
   for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
     const Bucket& b = c.buckets[bi];
+    cudaStream_t main_st = st;
+    (void)main_st;
+    cudaStream_t st = c.side[bi % c.side.size()];
     cudaEventRecord(c.bucket_ev[bi], st);
-    if (b.count == 0) continue;
+    if (b.count == 0) {
+      cudaEventRecord(c.bucket_ev_end[bi], st);
+      continue;
+    }
     EvalArgs a;
     std::memset(&a, 0, sizeof a);
     a.scens = (const DevScen*)c.b_scens.ptr;
@@ -421,8 +462,9 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     a.cursor = cursors + bi;
     a.rows = (gpb_row*)c.b_rows.ptr;
     a.error_flag = err_flag;
-    a.row_cycles = c.profile_rows ? (long long*)c.dev_buf(c.b_cycles, 8 * (size_t)c.n_rows)
+    a.row_cycles = c.profile_rows ? (long long*)c.dev_buf(c.b_cycles, 72 * (size_t)c.n_rows)
                                   : nullptr;
+    a.row_phase = a.row_cycles ? a.row_cycles + c.n_rows : nullptr;
     const int grid = std::min(grid_eval, (b.count + 3) / 4);
     cudaError_t e;
     if (b.policy == GPB_GPIPE || b.policy == GPB_VARUNA) {
@@ -472,9 +514,13 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
       e = launch_atlas(b.B, a, agrid, wpc, st);
     }
     if (e != cudaSuccess) return c.cuda_fail(e, "eval launch");
+    cudaEventRecord(c.bucket_ev_end[bi], st);
     ++launches;
   }
-  cudaEventRecord(c.bucket_ev[c.buckets.size()], st);
+  for (size_t k = 0; k < c.side.size(); ++k) {  // join
+    cudaEventRecord(c.side_done[k], c.side[k]);
+    cudaStreamWaitEvent(st, c.side_done[k], 0);
+  }
   cudaEventRecord(c.ev1, st);
   SelectArgs sa;
   sa.scens = (const DevScen*)c.b_scens.ptr;
@@ -574,7 +620,7 @@ int gpb_get_timing(gpb_ctx* ctx_, gpb_timing* out) {
     cudaEventElapsedTime(&out->select_ms, c.ev1, c.ev2);
     for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, c.bucket_ev[bi], c.bucket_ev[bi + 1]);
+      cudaEventElapsedTime(&ms, c.bucket_ev[bi], c.bucket_ev_end[bi]);
       out->policy_ms[c.buckets[bi].policy] += ms;
     }
   }
@@ -643,7 +689,9 @@ extern "C" int gpb_fetch_row_cycles(gpb_ctx* ctx_, int64_t* out, int64_t n) {
     return GPB_CONFIG_ERROR;
   }
   cudaSetDevice(c.device);
-  n = std::min(n, c.n_rows);
+  // out: n row costs followed by n x 4 atlas phase costs (when n == 5 * rows)
+  const int64_t rows = c.n_rows;
+  n = std::min(n, 9 * rows);
   cudaError_t e = cudaMemcpyAsync(out, c.b_cycles.ptr, 8 * (size_t)n, cudaMemcpyDeviceToHost,
                                   c.stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);

@@ -17,6 +17,8 @@ struct Buf {
   size_t bytes = 0;
 };
 
+constexpr size_t kSideStreams = 8;
+
 struct Bucket {
   int policy = 0;
   int B = 1;            // stages per lane = ceil(S / 32)
@@ -27,6 +29,7 @@ struct Bucket {
   int max_cm = 0;
   long long max_csm = 0;
   int max_c = 0, max_s = 0, max_nw = 0;
+  double cost = 0;  // estimated cost of the bucket's heaviest row
 };
 
 struct Ctx {
@@ -58,7 +61,10 @@ struct Ctx {
   Buf b_tl_rows, b_tl_spans, b_tl_nspan, b_tl_scratch, b_gaps, b_ngaps, b_reqs, b_pl,
       b_sum, b_pack_scratch, b_pack_misc;
 
-  std::vector<cudaEvent_t> bucket_ev;  // [buckets + 1]
+  std::vector<cudaEvent_t> bucket_ev;      // [buckets + 1] bucket start (+ fork)
+  std::vector<cudaEvent_t> bucket_ev_end;  // [buckets]
+  std::vector<cudaStream_t> side;          // concurrent bucket streams
+  std::vector<cudaEvent_t> side_done;
   Buf b_placements, b_ar;
   bool pack_allreduce = false;  // include the all-reduce tail in timelines
   // last build_timelines() outputs (device pointers into the buffers above)

@@ -26,6 +26,7 @@ struct EvalArgs {
   gpb_row* rows;              // output table
   int32_t* error_flag;
   long long* row_cycles;      // optional per-row clock64 cost (profiling)
+  long long* row_phase;       // optional [row][4] atlas phase cycles (profiling)
   // timeline variant: per-work-item offsets into forward-end / pair-start
   // arrays laid out [pipeline][stage][microbatch]
   long long* tl_fe;

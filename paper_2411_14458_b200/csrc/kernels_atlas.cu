@@ -38,10 +38,18 @@ constexpr int kAtlasQ = 2;  // commits per stage per wavefront round
 
 // ------------------------------------------------------- union of lists
 
-// first index i of a sorted start array with st[i] + len > x
+// first index i of a sorted start array with st[i] + len > x. Queries land
+// near the tail (reservations are made in time order), so probe backwards a
+// few entries before falling back to bisection.
 __device__ __forceinline__ int first_end_after(const long long* st, int n, long long len,
                                                long long x) {
-  int lo = 0, hi = n;
+  int i = n;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (i == 0 || st[i - 1] + len <= x) return i;
+    --i;
+  }
+  int lo = 0, hi = i;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if (st[mid] + len > x) hi = mid; else lo = mid + 1;
@@ -134,6 +142,52 @@ __device__ __forceinline__ long long union_latest_fit(const long long* base, int
   }
 }
 
+// free_at over the union, one lane per pipeline list (warp-uniform result).
+__device__ __forceinline__ bool warp_union_free_at(const long long* base, int C, int M,
+                                                   const LinkCounts& k, long long start,
+                                                   long long len) {
+  if (len <= 0) return true;
+  bool conflict = false;
+  for (int q = threadIdx.x & 31; q < C; q += 32) {
+    const int n = k.count(q);
+    if (n == 0) continue;
+    const long long* st = base + (size_t)q * M;
+    if (st[n - 1] + len <= start) continue;
+    const int i = first_end_after(st, n, len, start);
+    if (i < n && st[i] < start + len) conflict = true;
+  }
+  return !__any_sync(0xffffffffu, conflict);
+}
+
+// earliest_fit over the union: every lane pushes t past the overlapping run
+// of its own list; the warp max of the proposals keeps "no feasible start in
+// [lo, t)" invariant, and the fixpoint is the reference's answer.
+__device__ __forceinline__ long long warp_union_earliest_fit(const long long* base, int C, int M,
+                                                             const LinkCounts& k, long long lo,
+                                                             long long len) {
+  if (len <= 0) return lo;
+  long long t = lo;
+  for (;;) {
+    long long my = t;
+    for (int q = threadIdx.x & 31; q < C; q += 32) {
+      const int n = k.count(q);
+      if (n == 0) continue;
+      const long long* st = base + (size_t)q * M;
+      if (st[n - 1] + len <= my) continue;
+      int i = first_end_after(st, n, len, my);
+      while (i < n && st[i] < my + len) {
+        my = st[i] + len;
+        ++i;
+      }
+    }
+    long long nt = my;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nt = imax(nt, __shfl_xor_sync(0xffffffffu, nt, o));
+    if (nt == t) return t;
+    t = nt;
+  }
+}
+
 // ------------------------------------------------------------ the warp
 
 struct AtlasMem {
@@ -176,8 +230,11 @@ __device__ __forceinline__ long long atlas_cand(const Geom& g, const AtlasMem& X
 }
 
 template <int B, bool TIMELINE>
-__device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& err) {
+__device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& err,
+                               long long* phase = nullptr) {
   const int lane = threadIdx.x & 31;
+  long long ph_casc = 0, ph_chain = 0, ph_fit = 0, ph_drain = 0, ph_t = 0;
+  long long n_stage_it = 0, n_pairs = 0, n_adm = 0;
   const int S = g.S, M = g.M, C = g.C;
   const long long f = g.fwd, dur = g.dur;
   const int nw = g.nb - 1;
@@ -189,6 +246,10 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     int w;
     X.wbs[s] = (s > 0 && wan_after(g, s - 1, w)) ? w : -1;
     X.done[s] = 0;
+  }
+  if (lane < nw) {  // pooled serialization / latency per WAN boundary
+    X.wa[8 + lane] = g.ser_pooled[lane];
+    X.wg[8 + lane] = g.lat[lane];
   }
   __syncwarp();
 
@@ -226,33 +287,72 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
   }
 
   // ------------------------------------------------------ forward phase
+  // Per-lane registers for the current pipeline p: gpu_free and drained
+  // counts of the owned stages (written back to shared memory per p).
+  long long gfr[B];
+  int drr[B];
   for (int p = 0; p < C; ++p) {
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      gfr[j] = 0;
+      drr[j] = 0;
+    }
     for (int m = 0; m < M; ++m) {
       // memory-cap admission (:366-381) + forced drains (:321-346)
+      if (phase) ph_t = clock64();
       int nblk = 0;
 #pragma unroll
-      for (int j = 0; j < B; ++j) {
-        const int s = lane * B + j;
-        if (s < S && m - X.nm[p * S + s] >= mem_limit) ++nblk;
-      }
+      for (int j = 0; j < B; ++j)
+        if (lane * B + j < S && m - drr[j] >= mem_limit) ++nblk;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nblk += __shfl_xor_sync(kFull, nblk, o);
       if (nblk > 0) {
+        // The cascade is one descending pass over the stages; it runs in
+        // lane 0 on shared copies of this pipeline's state, forwarding the
+        // gradient just produced by the stage above in a register.
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          const int s = lane * B + j;
+          if (s < S) {
+            X.gf[p * S + s] = gfr[j];
+            X.nm[p * S + s] = drr[j];
+          }
+        }
+        __syncwarp();
         if (lane == 0) {
-          int nm_up = m;  // stage S-1: pair dm is ready iff forward dm is done
-          for (int s = S - 1; s >= 0 && nblk > 0; --s) {
-            const int i = p * S + s;
-            int dm = X.nm[i];
-            const int up = nm_up;
-            nm_up = dm;
-            if (dm >= M || dm >= up) continue;  // no ready pair
-            const int w = X.wbs[s];
-            const long long ser = w >= 0 ? g.ser_pooled[w] : 0;
-            const long long lat = w >= 0 ? g.lat[w] : 0;
-            long long gfi = X.gf[i];
-            while (dm < M && dm < up && nblk > 0) {
+          long long* __restrict__ gfp = X.gf + p * S;
+          int* __restrict__ nmp = X.nm + p * S;
+          long long* __restrict__ garr = X.garr;
+          const long long* __restrict__ fdl = X.fdl + p * M;
+          int nb = nblk, up = m, carry_m = -1;
+          long long carry = 0;
+          // software-pipelined: stage s-1's state is loaded while s drains
+          int n_dm = nmp[S - 1], n_w = X.wbs[S - 1];
+          long long n_gf = gfp[S - 1];
+          for (int s = S - 1; s >= 0 && nb > 0; --s) {
+            int dm = n_dm;
+            const int w = n_w;
+            long long gfi = n_gf;
+            if (s > 0) {
+              n_dm = nmp[s - 1];
+              n_w = X.wbs[s - 1];
+              n_gf = gfp[s - 1];
+            }
+            const int u = up;
+            up = dm;
+            ++n_stage_it;
+            if (dm >= M || dm >= u) {  // no ready pair: nothing new for s-1
+              carry_m = -1;
+              continue;
+            }
+            const long long ser = w >= 0 ? X.wa[8 + w] : 0;  // boundary constants
+            const long long lat = w >= 0 ? X.wg[8 + w] : 0;
+            long long produced = 0;
+            int pm = -1;
+            while (dm < M && dm < u && nb > 0) {
               const long long ready =
-                  s == S - 1 ? X.fdl[p * M + dm] : X.garr[((size_t)p * S + s) * M + dm];
+                  s == S - 1 ? fdl[dm]
+                             : (dm == carry_m ? carry : garr[((size_t)p * S + s) * M + dm]);
               const long long lo = imax(ready, gfi);
               long long t = lo;
               if (w >= 0) {
@@ -263,30 +363,48 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
               }
               const long long e = t + dur;  // atlas_commit_pair (:298-317)
               gfi = imax(gfi, e);
-              if (s > 0) X.garr[((size_t)p * S + s - 1) * M + dm] = w >= 0 ? e + ser + lat : e;
+              produced = w >= 0 ? e + ser + lat : e;
+              pm = dm;
+              if (s > 0) garr[((size_t)p * S + s - 1) * M + dm] = produced;
               if (TIMELINE) X.ps[((size_t)p * S + s) * M + dm] = t;
-              if (m - dm >= mem_limit && m - (dm + 1) < mem_limit) --nblk;
+              if (m - dm >= mem_limit && m - (dm + 1) < mem_limit) --nb;
               ++dm;
+              ++n_pairs;
             }
-            X.gf[i] = gfi;
-            X.nm[i] = dm;
-            nm_up = dm;
+            gfp[s] = gfi;
+            nmp[s] = dm;
+            up = dm;
+            carry = produced;
+            carry_m = pm;
           }
-          if (nblk > 0) X.done[0] = -1;  // DeadlockError marker (unreachable)
+          X.done[0] = nb;  // > 0: DeadlockError (unreachable)
+          ++n_adm;
         }
         __syncwarp();
-        if (X.done[0] == -1) {
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          const int s = lane * B + j;
+          if (s < S) {
+            gfr[j] = X.gf[p * S + s];
+            drr[j] = X.nm[p * S + s];
+          }
+        }
+        if (X.done[0] > 0) {
           err = 1;
           return 0;
         }
+      }
+      if (phase) {
+        const long long t1 = clock64();
+        ph_casc += t1 - ph_t;
+        ph_t = t1;
       }
       // chain: G_s prefix max (lane-local, then warp inclusive scan)
       long long gl[B];
       long long runmax = -kInf64;
 #pragma unroll
       for (int j = 0; j < B; ++j) {
-        const int s = lane * B + j;
-        if (s < S) runmax = imax(runmax, X.gf[p * S + s] - a_loc[j]);
+        if (lane * B + j < S) runmax = imax(runmax, gfr[j] - a_loc[j]);
         gl[j] = runmax;
       }
       long long pre = runmax;
@@ -307,41 +425,60 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
           X.wg[w] = gl[j];
         }
       }
+      long long t0 = __shfl_sync(kFull, gfr[0], 0);  // gpu_free of stage 0
       __syncwarp();
-      // exact-fit shift loop over the WAN boundaries (:383-405) and the
-      // activation reservations of the committed chain (:407-430)
-      long long t0 = X.gf[p * S + 0];
-      if (lane == 0) {
+      if (phase) {
+        const long long t1 = clock64();
+        ph_chain += t1 - ph_t;
+        ph_t = t1;
+      }
+      // exact-fit shift loop over the WAN boundaries (:383-405), one lane per
+      // pipeline list of each link, then the chain's reservations (:407-430)
+      {
         LinkCounts k{nullptr, S, 0, p, m, 1, M};
         for (int w = 0; w < nw;) {
           const long long e = X.wa[w] + f + imax(t0, X.wg[w]);
           const long long* base = X.resf + (size_t)w * C * M;
           const long long len = g.ser_pooled[w];
-          if (!union_free_at(base, C, M, k, e, len)) {
-            t0 += union_earliest_fit(base, C, M, k, e, len) - e;
+          if (!warp_union_free_at(base, C, M, k, e, len)) {
+            t0 += warp_union_earliest_fit(base, C, M, k, e, len) - e;
             w = 0;  // restart the chain
           } else {
             ++w;
           }
         }
-        for (int w = 0; w < nw; ++w)
-          X.resf[((size_t)w * C + p) * M + m] = X.wa[w] + f + imax(t0, X.wg[w]);
+        if (lane < nw)
+          X.resf[((size_t)lane * C + p) * M + m] = X.wa[lane] + f + imax(t0, X.wg[lane]);
       }
-      t0 = __shfl_sync(kFull, t0, 0);
+      if (phase) {
+        const long long t1 = clock64();
+        ph_fit += t1 - ph_t;
+        ph_t = t1;
+      }
 #pragma unroll
       for (int j = 0; j < B; ++j) {
         const int s = lane * B + j;
         if (s < S) {
           const long long e = a_loc[j] + f + imax(t0, gl[j]);
-          X.gf[p * S + s] = e;
+          gfr[j] = e;
           if (s == S - 1) X.fdl[p * M + m] = e;
           if (TIMELINE) X.fe[((size_t)p * S + s) * M + m] = e;
         }
       }
       __syncwarp();
     }
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const int s = lane * B + j;
+      if (s < S) {
+        X.gf[p * S + s] = gfr[j];
+        X.nm[p * S + s] = drr[j];
+      }
+    }
+    __syncwarp();
   }
 
+  if (phase) ph_t = clock64();
   // ------------------------------------------ drain: per-stage wavefront
 #pragma unroll
   for (int j = 0; j < B; ++j) {
@@ -443,6 +580,16 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     __syncwarp();
   }
 
+  if (phase && lane == 0) {
+    ph_drain = clock64() - ph_t;
+    phase[0] = ph_casc;
+    phase[1] = ph_chain;
+    phase[2] = ph_fit;
+    phase[3] = ph_drain;
+    phase[4] = n_stage_it;
+    phase[5] = n_pairs;
+    phase[6] = n_adm;
+  }
   // -------------------------------------------- right-pack (timeline)
   if (TIMELINE) {
     if (lane == 0) {
@@ -499,7 +646,8 @@ __global__ void __launch_bounds__(kEvalThreads) atlas_kernel(EvalArgs a) {
     const DevTopo* tp;
     if (!begin_row(a, row, g, sc, tp)) continue;
     int err = 0;
-    const long long mk = atlas_row<B, false>(g, sc->mem_limit, X, err);
+    const long long mk = atlas_row<B, false>(g, sc->mem_limit, X, err,
+                                             a.row_phase ? a.row_phase + 8 * (size_t)row : nullptr);
     end_row(a, row, g, *sc, *tp, mk, err, t_start);
     __syncwarp();
   }

@@ -16,10 +16,14 @@ n = p.load(abi.array(abi.Topology, topos), abi.array(abi.Scenario, scens))
 p.evaluate()
 p.evaluate()
 rows = p.rows()
-cyc = p.row_cycles()
+import ctypes as C
+raw = (C.c_int64 * (9 * n))()
+p._check(p.lib.gpb_fetch_row_cycles(p.ctx, raw, 9 * n))
+cyc = list(raw[:n])
+phase = [list(raw[n + 8 * i: n + 8 * i + 8]) for i in range(n)]
 t = p.timing()
-agg = collections.defaultdict(lambda: [0, 0, 0])
-for r, c in zip(rows[:n], cyc):
+agg = collections.defaultdict(lambda: [0, 0, 0, [0] * 8])
+for r, c, ph in zip(rows[:n], cyc, phase):
     s = scens[r.scenario]
     S = (s.num_layers + s.layers_per_partition - 1) // s.layers_per_partition
     key = (abi.POLICY_NAMES[s.policy], S, s.pipelines_per_cell, s.num_microbatches, r.feasible)
@@ -27,8 +31,13 @@ for r, c in zip(rows[:n], cyc):
     a[0] += 1
     a[1] += c
     a[2] = max(a[2], c)
+    if s.policy == 3:
+        for k in range(8):
+            a[3][k] += ph[k]
 tot = sum(v[1] for v in agg.values())
 print(json.dumps({"evaluate_ms": t.evaluate_ms, "policy_ms": list(t.policy_ms)}))
 print("policy S C M feas | rows  sum_Mcyc  share  max_kcyc")
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:25]:
-    print(*k, "|", v[0], round(v[1] / 1e6, 2), f"{100 * v[1] / tot:.1f}%", round(v[2] / 1e3, 1))
+    ph = [round(x / max(1, v[1]) * 100) for x in v[3][:4]] + [round(x / v[0]) for x in v[3][4:7]]
+    print(*k, "|", v[0], round(v[1] / 1e6, 2), f"{100 * v[1] / tot:.1f}%", round(v[2] / 1e3, 1),
+          "phases% casc/chain/fit/drain + per-row stage_it/pairs/adm", ph)
