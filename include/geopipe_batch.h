@@ -271,6 +271,16 @@ int gpb_microbench(gpb_ctx* ctx, int32_t kind, double* gops);
 int gpb_set_profile(gpb_ctx* ctx, int32_t enable);
 int gpb_fetch_row_cycles(gpb_ctx* ctx, int64_t* out, int64_t n);
 
+/* Profiling: the last gpb_evaluate's row buckets (one kernel launch each, on
+ * concurrent streams) with their shapes and device times. Writes
+ * min(n, cap) records; *n = number of buckets. */
+typedef struct gpb_bucket_info {
+  int32_t policy, B, rows, max_s, max_c, max_m, stream, pad_;
+  float start_ms;              /* launch-stream fork -> bucket start */
+  float ms;                    /* bucket kernel duration */
+} gpb_bucket_info;
+int gpb_bucket_infos(gpb_ctx* ctx, gpb_bucket_info* out, int32_t cap, int32_t* n);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -91,6 +91,13 @@ class ScenarioResult(C.Structure):
     ]
 
 
+class BucketInfo(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("B", C.c_int32), ("rows", C.c_int32),
+                ("max_s", C.c_int32), ("max_c", C.c_int32), ("max_m", C.c_int32),
+                ("stream", C.c_int32), ("pad_", C.c_int32), ("start_ms", C.c_float),
+                ("ms", C.c_float)]
+
+
 class Best(C.Structure):
     _fields_ = [("throughput", C.c_double), ("row", C.c_int64)]
 

@@ -11,11 +11,12 @@ namespace gpb {
 struct AtlasLayout {
   // inputs
   int C, S, M, nw;     // nw = max WAN boundaries (<= 7)
-  bool garr_in_smem;
+  long long garr_cap;  // gradient-queue entries kept in shared memory per warp
+                       // (rows with C*S*M above it use the global scratch)
   // outputs
   size_t off_wa, off_wg, off_wbs, off_gf, off_cand, off_lastc, off_nm, off_done,
       off_firstm, off_pub_nm, off_pub_last, off_pub_done, off_fdl, off_resf, off_resb,
-      off_garr, total;
+      off_hint, off_garr, total;
   int cap;             // list storage per WAN boundary = C * M (C lists of M)
 
   __host__ __device__ static size_t al(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -39,8 +40,9 @@ struct AtlasLayout {
     off_fdl = o;       o = al(o + (size_t)C * M * 8);
     off_resf = o;      o = al(o + (size_t)nw * cap * 8);
     off_resb = o;      o = al(o + (size_t)nw * cap * 8);
+    off_hint = o;      o = al(o + (size_t)2 * (nw > 0 ? nw : 1) * C * 4);  // search cursors
     off_garr = o;
-    if (garr_in_smem) o = al(o + CS * M * 8);
+    o = al(o + (size_t)garr_cap * 8);
     total = o;
   }
 };

@@ -639,28 +639,19 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
       a.smem_m = g.max_m;
       e = launch_timeline(g.policy, g.B, a, std::min(c.num_sms * 8, (g.cnt + 3) / 4), st);
     } else {
-      AtlasLayout L;
-      L.C = g.max_c;
-      L.S = g.max_s;
-      L.M = g.max_m;
-      L.nw = g.max_nw;
-      L.garr_in_smem = true;
-      L.compute();
-      if (L.total * 4 > 220 * 1024) {
-        L.garr_in_smem = false;
-        L.compute();
-      }
-      const int wpc = (int)std::min<size_t>(4, (size_t)c.smem_optin / L.total);
-      if (wpc < 1) {
-        c.set_error("atlas plan too large for the shared-memory slice");
-        return GPB_CONFIG_ERROR;
-      }
-      a.lay = L;
-      const int grid = std::min(c.num_sms * 4, (g.cnt + wpc - 1) / wpc);
-      if (!L.garr_in_smem) {
-        a.scratch_per_warp = (long long)L.C * L.S * L.M;
+      AtlasPlan P;
+      long long max_csm = 0;
+      const int rc = plan_atlas(c, g.B, true, g.max_c, g.max_s, g.max_m, g.max_nw,
+                                (long long)g.max_c * g.max_s * g.max_m, g.cnt, P);
+      (void)max_csm;
+      if (rc != GPB_OK) return rc;
+      a.lay = P.L;
+      const int grid = P.grid, wpc = P.wpc;
+      a.scratch = nullptr;
+      a.scratch_per_warp = P.scratch_per_warp;
+      if (P.scratch_per_warp > 0) {
         a.scratch = (long long*)c.dev_buf(c.b_tl_scratch,
-                                          8 * (size_t)a.scratch_per_warp * grid * wpc);
+                                          8 * (size_t)P.scratch_per_warp * grid * wpc);
         if (!a.scratch) return c.cuda_fail(cudaErrorMemoryAllocation, "atlas scratch");
       }
       e = launch_atlas_timeline(g.B, a, grid, wpc, st);

@@ -328,31 +328,39 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   // Buckets: (policy, B = ceil(S/32)); within a bucket scenarios are dealt
   // in decreasing estimated cost so the persistent warps finish together.
   c.buckets.clear();
-  // ATLAS rows are further split by the size class of their shared-memory
-  // slice (log2 of C*S*M) so small rows are not sized for the largest one.
+  // One bucket (one kernel) per (policy, B): rows of every shape share the
+  // persistent warps, heaviest first. Estimated row cost in clock cycles
+  // (fitted to profiled config-2 rows): ATLAS ~ C*M*(2000*C + 250*S) (list
+  // unions over C pipelines + per-pair work), the flush/1F1B wavefronts
+  // ~ 20*M*S.
+  // ATLAS rows within 30% of the heaviest estimate form their own "heavy"
+  // bucket, launched first (few warps, the critical path); the short
+  // flush/1F1B buckets follow, then the bulk ATLAS rows fill the GPU.
+  auto cost = [&](int i) {
+    const DevScen& d = ds[i];
+    return d.policy == GPB_ATLAS ? (double)d.C * d.M * (2000.0 * d.C + 250.0 * d.S)
+                                 : 20.0 * d.M * d.S;
+  };
+  double max_atlas = 0;
+  for (int i = 0; i < n_scen; ++i)
+    if (ds[i].policy == GPB_ATLAS) max_atlas = std::max(max_atlas, cost(i));
   std::map<std::tuple<int, int, int>, std::vector<int>> by_key;
   for (int i = 0; i < n_scen; ++i) {
-    int cls = 0;
-    if (ds[i].policy == GPB_ATLAS) {
-      const long long csm = (long long)ds[i].C * ds[i].S * ds[i].M;
-      while ((1LL << cls) < csm) ++cls;
-    }
-    by_key[{ds[i].policy, (ds[i].S + 31) / 32, cls}].push_back(i);
+    const int heavy = ds[i].policy == GPB_ATLAS && cost(i) >= 0.3 * max_atlas;
+    by_key[{ds[i].policy, (ds[i].S + 31) / 32, heavy}].push_back(i);
   }
   std::vector<int32_t> work;
   work.reserve(n_rows);
   for (auto& [key, list] : by_key) {
-    auto cost = [&](int i) {
-      const DevScen& d = ds[i];
-      double base = (double)d.M * d.S;
-      return d.policy == GPB_ATLAS ? base * d.C * d.C : base;
-    };
     std::stable_sort(list.begin(), list.end(), [&](int a, int b) { return cost(a) > cost(b); });
     Bucket b;
     b.policy = std::get<0>(key);
     b.B = std::get<1>(key);
+    b.heavy = std::get<2>(key) != 0;
     b.offset = (int32_t)work.size();
+    double total = 0;
     for (int i : list) {
+      total += cost(i) * ds[i].n_rows;
       for (int k = 0; k < ds[i].n_rows; ++k) work.push_back((int32_t)(ds[i].first_row + k));
       b.max_m = std::max(b.max_m, ds[i].M);
       b.max_cs = std::max(b.max_cs, ds[i].C * ds[i].S);
@@ -364,11 +372,16 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
     }
     b.count = (int32_t)work.size() - b.offset;
     b.cost = cost(list.front());
+    // makespan estimate: the longest row, or the whole bucket spread over
+    // ~8 resident warps per SM
+    b.est = std::max(b.cost, total / (8.0 * std::max(1, c.num_sms)));
     c.buckets.push_back(b);
   }
-  // longest rows first: their buckets are launched first on the side streams
-  std::stable_sort(c.buckets.begin(), c.buckets.end(),
-                   [](const Bucket& x, const Bucket& y) { return x.cost > y.cost; });
+  // launch order: heavy ATLAS, flush/1F1B, bulk ATLAS; heaviest first within
+  auto rank = [](const Bucket& b) { return b.policy != GPB_ATLAS ? 1 : (b.heavy ? 0 : 2); };
+  std::stable_sort(c.buckets.begin(), c.buckets.end(), [&](const Bucket& x, const Bucket& y) {
+    return rank(x) != rank(y) ? rank(x) < rank(y) : x.cost > y.cost;
+  });
 
   // Upload (one H2D per table).
   cudaStream_t st = c.stream;
@@ -425,8 +438,11 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     if (cudaEventCreate(&e) != cudaSuccess) return c.cuda_fail(cudaGetLastError(), "event");
     c.bucket_ev.push_back(e);
   }
-  // buckets run concurrently on side streams forked from the launch stream
-  while (c.side.size() < kSideStreams) {
+  // buckets run concurrently on side streams forked from the launch stream:
+  // one stream per bucket up to kSideStreams, beyond that longest-first
+  // onto the least loaded stream
+  const size_t n_side = std::max<size_t>(1, std::min<size_t>(kSideStreams, c.buckets.size()));
+  while (c.side.size() < n_side) {
     cudaStream_t s2;
     cudaEvent_t e2;
     if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess ||
@@ -441,12 +457,43 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     c.bucket_ev_end.push_back(e);
   }
   cudaEventRecord(c.bucket_ev[c.buckets.size()], st);  // fork point
-  for (size_t k = 0; k < c.side.size(); ++k) cudaStreamWaitEvent(c.side[k], c.bucket_ev[c.buckets.size()], 0);
+  for (size_t k = 0; k < n_side; ++k) cudaStreamWaitEvent(c.side[k], c.bucket_ev[c.buckets.size()], 0);
+  // ATLAS launch shapes first: the global gradient-queue scratch of every
+  // concurrently running bucket is carved from one allocation
+  std::vector<AtlasPlan> aplan(c.buckets.size());
+  std::vector<size_t> scr_off(c.buckets.size(), 0);
+  size_t scr_total = 0;
   for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
     const Bucket& b = c.buckets[bi];
-    cudaStream_t main_st = st;
-    (void)main_st;
-    cudaStream_t st = c.side[bi % c.side.size()];
+    if (b.policy != GPB_ATLAS || b.count == 0) continue;
+    const int rc = plan_atlas(c, b.B, false, b.max_c, b.max_s, b.max_m, b.max_nw, b.max_csm,
+                              b.count, aplan[bi]);
+    if (rc != GPB_OK) return rc;
+    if (std::getenv("GPB_DEBUG_PLAN"))
+      std::fprintf(stderr, "atlas bucket %zu B=%d rows=%d C=%d S=%d M=%d nw=%d csm=%lld cap=%lld "
+                   "total=%zu wpc=%d grid=%d spw=%lld\n", bi, b.B, b.count, b.max_c, b.max_s,
+                   b.max_m, b.max_nw, b.max_csm, aplan[bi].L.garr_cap, aplan[bi].L.total,
+                   aplan[bi].wpc, aplan[bi].grid, aplan[bi].scratch_per_warp);
+    scr_off[bi] = scr_total;
+    scr_total += (size_t)aplan[bi].scratch_per_warp * aplan[bi].grid * aplan[bi].wpc;
+  }
+  if (scr_total > 0 && !c.dev_buf(c.b_scratch, sizeof(long long) * scr_total))
+    return c.cuda_fail(cudaErrorMemoryAllocation, "atlas scratch");
+  {  // streams: longest estimate first onto the least loaded stream (LPT)
+    std::vector<size_t> ord(c.buckets.size());
+    for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](size_t x, size_t y) { return c.buckets[x].est > c.buckets[y].est; });
+    std::vector<double> load(n_side, 0.0);
+    for (size_t i : ord) {
+      const size_t si = std::min_element(load.begin(), load.end()) - load.begin();
+      load[si] += c.buckets[i].est;
+      c.buckets[i].stream = (int)si;
+    }
+  }
+  for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
+    const Bucket& b = c.buckets[bi];
+    cudaStream_t st = c.side[b.stream];
     cudaEventRecord(c.bucket_ev[bi], st);
     if (b.count == 0) {
       cudaEventRecord(c.bucket_ev_end[bi], st);
@@ -478,46 +525,18 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     } else if (b.policy == GPB_1F1B) {
       e = launch_onef1b(b.B, a, grid, st);
     } else {
-      // per-warp shared slice. ATLAS rows are latency-bound per warp and the
-      // longest row sets the kernel time, so the gradient queues stay in
-      // shared memory whenever 4 warps per SM still fit (measured faster than
-      // higher occupancy with L1/L2-resident queues), else they go global.
-      AtlasLayout L;
-      L.C = b.max_c;
-      L.S = b.max_s;
-      L.M = b.max_m;
-      L.nw = b.max_nw;
-      L.garr_in_smem = true;
-      L.compute();
-      const size_t sm_budget = 220 * 1024;
-      if (L.total * 4 > sm_budget) {
-        L.garr_in_smem = false;
-        L.compute();
-      }
-      int wpc = (int)std::min<size_t>(4, (size_t)c.smem_optin / L.total);
-      if (wpc < 1) {
-        c.set_error("atlas plan too large for the shared-memory slice");
-        return GPB_CONFIG_ERROR;
-      }
-      a.lay = L;
-      const int per_sm = std::max(1, (int)std::min<size_t>(64 / wpc, sm_budget / (L.total * wpc)));
-      const int agrid = std::min(c.num_sms * per_sm, (b.count + wpc - 1) / wpc);
-      a.scratch = nullptr;
-      a.scratch_per_warp = 0;
-      if (!L.garr_in_smem) {
-        a.scratch_per_warp = (long long)L.C * L.S * L.M;
-        void* scr = c.dev_buf(c.b_scratch, sizeof(long long) * a.scratch_per_warp *
-                                               (size_t)agrid * wpc);
-        if (!scr) return c.cuda_fail(cudaErrorMemoryAllocation, "atlas scratch");
-        a.scratch = (long long*)scr;
-      }
+      const AtlasPlan& P = aplan[bi];
+      a.lay = P.L;
+      a.scratch_per_warp = P.scratch_per_warp;
+      a.scratch = P.scratch_per_warp > 0 ? (long long*)c.b_scratch.ptr + scr_off[bi] : nullptr;
+      const int agrid = P.grid, wpc = P.wpc;
       e = launch_atlas(b.B, a, agrid, wpc, st);
     }
     if (e != cudaSuccess) return c.cuda_fail(e, "eval launch");
     cudaEventRecord(c.bucket_ev_end[bi], st);
     ++launches;
   }
-  for (size_t k = 0; k < c.side.size(); ++k) {  // join
+  for (size_t k = 0; k < n_side; ++k) {  // join
     cudaEventRecord(c.side_done[k], c.side[k]);
     cudaStreamWaitEvent(st, c.side_done[k], 0);
   }
@@ -601,6 +620,30 @@ int gpb_set_stream(gpb_ctx* ctx_, void* s) {
   if (!ctx_) return GPB_ERROR;
   Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
   c.stream = s ? (cudaStream_t)s : c.own_stream;
+  return GPB_OK;
+}
+
+int gpb_bucket_infos(gpb_ctx* ctx_, gpb_bucket_info* out, int32_t cap, int32_t* n) {
+  if (!ctx_ || !n || (cap > 0 && !out)) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  *n = (int32_t)c.buckets.size();
+  if (c.timing_valid) cudaEventSynchronize(c.ev2);
+  for (int32_t bi = 0; bi < std::min<int32_t>(cap, *n); ++bi) {
+    const Bucket& b = c.buckets[bi];
+    gpb_bucket_info& o = out[bi];
+    std::memset(&o, 0, sizeof o);
+    o.policy = b.policy;
+    o.B = b.B;
+    o.rows = b.count;
+    o.max_s = b.max_s;
+    o.max_c = b.max_c;
+    o.max_m = b.max_m;
+    o.stream = b.stream;
+    if (c.timing_valid) {
+      cudaEventElapsedTime(&o.start_ms, c.bucket_ev[c.buckets.size()], c.bucket_ev[bi]);
+      cudaEventElapsedTime(&o.ms, c.bucket_ev[bi], c.bucket_ev_end[bi]);
+    }
+  }
   return GPB_OK;
 }
 
@@ -697,3 +740,45 @@ extern "C" int gpb_fetch_row_cycles(gpb_ctx* ctx_, int64_t* out, int64_t n) {
   if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
   return e == cudaSuccess ? GPB_OK : c.cuda_fail(e, "fetch row cycles");
 }
+
+namespace gpb {
+
+// ATLAS launch shape. The per-warp shared slice holds the reservation lists,
+// the per-pipeline stage state and the last-stage forward ends; the gradient
+// queues [C][S][M] go to a per-warp global scratch (L1/L2-resident). Measured
+// on config 2: global queues with 12 warps/SM beat shared-memory queues at
+// 4-8 warps/SM both for the bucket makespan and for the longest row (the
+// stage-strided queue accesses conflict on shared-memory banks).
+// GPB_ATLAS_GARR_SMEM=<warps per SM> keeps queues that fit in shared memory
+// at that occupancy (experiments).
+int plan_atlas(Ctx& c, int B, bool timeline, int C, int S, int M, int nw, long long max_csm,
+               long long count, AtlasPlan& P) {
+  const size_t sm_budget = 220 * 1024;
+  AtlasLayout& L = P.L;
+  L.C = C;
+  L.S = S;
+  L.M = M;
+  L.nw = nw;
+  L.garr_cap = 0;
+  L.compute();
+  if (const char* t = std::getenv("GPB_ATLAS_GARR_SMEM")) {
+    const long long target = std::max(1, std::atoi(t));
+    const long long room = ((long long)(sm_budget / target) - (long long)L.total) / 8;
+    L.garr_cap = std::max(0LL, std::min(max_csm, room));
+    L.compute();
+  }
+  P.wpc = (int)std::min<size_t>(4, (size_t)c.smem_optin / L.total);
+  if (P.wpc < 1) {
+    c.set_error("atlas plan too large for the shared-memory slice");
+    return GPB_CONFIG_ERROR;
+  }
+  const size_t smem = (size_t)P.wpc * L.total;
+  int per_sm = atlas_blocks_per_sm(B, timeline, P.wpc, smem);
+  per_sm = std::max(1, std::min(per_sm, (int)(sm_budget / smem)));
+  P.grid = (int)std::max(1LL, std::min<long long>((long long)c.num_sms * per_sm,
+                                                  (count + P.wpc - 1) / P.wpc));
+  P.scratch_per_warp = L.garr_cap < max_csm ? max_csm : 0;
+  return GPB_OK;
+}
+
+}  // namespace gpb

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../include/geopipe_batch.h"
+#include "atlas_layout.h"
 #include "device_common.cuh"
 
 namespace gpb {
@@ -17,6 +18,8 @@ struct Buf {
   size_t bytes = 0;
 };
 
+// The device exposes CUDA_DEVICE_MAX_CONNECTIONS (default 8) hardware work
+// queues; more streams alias onto them and serialize unrelated buckets.
 constexpr size_t kSideStreams = 8;
 
 struct Bucket {
@@ -29,7 +32,10 @@ struct Bucket {
   int max_cm = 0;
   long long max_csm = 0;
   int max_c = 0, max_s = 0, max_nw = 0;
+  double est = 0;   // estimated bucket makespan (same units as cost)
   double cost = 0;  // estimated cost of the bucket's heaviest row
+  int stream = 0;   // side stream it ran on
+  bool heavy = false;  // ATLAS rows near the heaviest estimate (launched first)
 };
 
 struct Ctx {
@@ -89,5 +95,15 @@ struct Ctx {
   int check_error_flag();
   ~Ctx();
 };
+
+// Launch shape of one ATLAS kernel (evaluation or timeline variant) over
+// `count` rows whose largest C, S, M, WAN count and C*S*M are given.
+struct AtlasPlan {
+  AtlasLayout L;
+  int wpc = 0, grid = 0;
+  long long scratch_per_warp = 0;  // global gradient-queue entries per warp
+};
+int plan_atlas(Ctx& c, int B, bool timeline, int C, int S, int M, int nw, long long max_csm,
+               long long count, AtlasPlan& P);
 
 }  // namespace gpb

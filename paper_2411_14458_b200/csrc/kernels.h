@@ -52,6 +52,7 @@ struct SelectArgs {
 cudaError_t launch_flush(int B, bool gpipe, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_onef1b(int B, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_atlas(int B, const EvalArgs& a, int grid, int wpc, cudaStream_t st);
+int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem);
 cudaError_t launch_select(const SelectArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_timeline(int policy, int B, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_atlas_timeline(int B, const EvalArgs& a, int grid, int wpc, cudaStream_t st);

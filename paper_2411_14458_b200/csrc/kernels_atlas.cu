@@ -38,22 +38,40 @@ constexpr int kAtlasQ = 2;  // commits per stage per wavefront round
 
 // ------------------------------------------------------- union of lists
 
-// first index i of a sorted start array with st[i] + len > x. Queries land
-// near the tail (reservations are made in time order), so probe backwards a
-// few entries before falling back to bisection.
+// first index i of a sorted start array with st[i] + len > x. Queries on one
+// link arrive in nearly increasing time order, so the search starts at the
+// per-(link, pipeline) cursor `h` (when given) and walks a few entries
+// either way before falling back to bisection; the cursor is updated.
 __device__ __forceinline__ int first_end_after(const long long* st, int n, long long len,
-                                               long long x) {
-  int i = n;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (i == 0 || st[i - 1] + len <= x) return i;
-    --i;
+                                               long long x, int* h = nullptr) {
+  int lo = 0, hi = n;
+  int i = h ? max(0, min(*h, n)) : n;
+  if (i > 0 && st[i - 1] + len > x) {  // answer < i: walk back
+    hi = i - 1;
+#pragma unroll 1
+    for (int k = 0; k < 6; ++k) {
+      if (hi == 0 || st[hi - 1] + len <= x) {
+        lo = hi;
+        break;
+      }
+      --hi;
+    }
+  } else {  // answer >= i: walk forward
+    lo = i;
+#pragma unroll 1
+    for (int k = 0; k < 6; ++k) {
+      if (lo == n || st[lo] + len > x) {
+        hi = lo;
+        break;
+      }
+      ++lo;
+    }
   }
-  int lo = 0, hi = i;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if (st[mid] + len > x) hi = mid; else lo = mid + 1;
   }
+  if (h) *h = lo;
   return lo;
 }
 
@@ -64,6 +82,8 @@ struct LinkCounts {
   int p, m;        // pipeline whose count is overridden by m (-1: none)
   int mode;        // 0: res_bwd counts from nm; 1: res_fwd (q<p: M, q==p: m)
   int M;
+  int* hint;       // per-pipeline search cursors of this link, or nullptr
+  __device__ __forceinline__ int* cur(int q) const { return hint ? hint + q : nullptr; }
   __device__ __forceinline__ int count(int q) const {
     if (mode == 1) return q < p ? M : (q == p ? m : 0);
     return q == p ? m : nm[q * S + s];
@@ -83,7 +103,7 @@ __device__ __forceinline__ long long union_earliest_fit(const long long* base, i
       if (n == 0) continue;
       const long long* st = base + (size_t)q * M;
       if (st[n - 1] + len <= t) continue;
-      int i = first_end_after(st, n, len, t);
+      int i = first_end_after(st, n, len, t, k.cur(q));
       while (i < n && st[i] < t + len) {
         t = st[i] + len;
         ++i;
@@ -104,7 +124,7 @@ __device__ __forceinline__ bool union_free_at(const long long* base, int C, int 
     if (n == 0) continue;
     const long long* st = base + (size_t)q * M;
     if (st[n - 1] + len <= start) continue;
-    const int i = first_end_after(st, n, len, start);
+    const int i = first_end_after(st, n, len, start, k.cur(q));
     if (i < n && st[i] < start + len) return false;
   }
   return true;
@@ -153,7 +173,7 @@ __device__ __forceinline__ bool warp_union_free_at(const long long* base, int C,
     if (n == 0) continue;
     const long long* st = base + (size_t)q * M;
     if (st[n - 1] + len <= start) continue;
-    const int i = first_end_after(st, n, len, start);
+    const int i = first_end_after(st, n, len, start, k.cur(q));
     if (i < n && st[i] < start + len) conflict = true;
   }
   return !__any_sync(0xffffffffu, conflict);
@@ -174,7 +194,7 @@ __device__ __forceinline__ long long warp_union_earliest_fit(const long long* ba
       if (n == 0) continue;
       const long long* st = base + (size_t)q * M;
       if (st[n - 1] + len <= my) continue;
-      int i = first_end_after(st, n, len, my);
+      int i = first_end_after(st, n, len, my, k.cur(q));
       while (i < n && st[i] < my + len) {
         my = st[i] + len;
         ++i;
@@ -192,7 +212,9 @@ __device__ __forceinline__ long long warp_union_earliest_fit(const long long* ba
 
 struct AtlasMem {
   long long *wa, *wg, *gf, *cand, *lastc, *fdl, *resf, *resb, *garr, *pub_last;
-  int *wbs, *nm, *done, *firstm, *pub_nm, *pub_done;
+  long long *garr_smem, *garr_glob;
+  long long garr_cap;
+  int *wbs, *nm, *done, *firstm, *pub_nm, *pub_done, *hintf, *hintb;
   long long* fe;  // timeline: forward ends [C][S][M] (global)
   long long* ps;  // timeline: pair starts  [C][S][M] (global)
 
@@ -212,7 +234,12 @@ struct AtlasMem {
     fdl = (long long*)(base + L.off_fdl);
     resf = (long long*)(base + L.off_resf);
     resb = (long long*)(base + L.off_resb);
-    garr = L.garr_in_smem ? (long long*)(base + L.off_garr) : garr_global;
+    hintf = (int*)(base + L.off_hint);
+    hintb = hintf + (L.nw > 0 ? L.nw : 1) * L.C;
+    garr_smem = (long long*)(base + L.off_garr);
+    garr_glob = garr_global;
+    garr_cap = L.garr_cap;
+    garr = garr_smem;
     fe = ps = nullptr;
   }
 };
@@ -225,8 +252,177 @@ __device__ __forceinline__ long long atlas_cand(const Geom& g, const AtlasMem& X
   const long long ready = s == S - 1 ? X.fdl[p * M + m] : X.garr[((size_t)p * S + s) * M + m];
   const long long lo = imax(ready, X.gf[p * S + s]);
   if (wb < 0) return lo;
-  LinkCounts k{X.nm, S, s, -1, 0, 0, M};
+  LinkCounts k{X.nm, S, s, -1, 0, 0, M, X.hintb + wb * C};
   return union_earliest_fit(X.resb + (size_t)wb * C * M, C, M, k, lo + g.dur, serb) - g.dur;
+}
+
+// ------------------------------------------------ admission cascade
+//
+// The memory-cap admission of microbatch m of pipeline p (scheduler.cpp:
+// 366-381) repeats atlas_drain_step (:321-346) — "drain the deepest stage
+// with a ready pair" — while some stage s has m - drained[s] >= mem_limit.
+// Stage S-1 has every forwarded pair ready; a stage's ready pairs come only
+// from the stage above, so the repetition is one descending pass in which
+// every stage above the lowest blocked stage s_min drains ALL its ready
+// pairs (up to pair m-1, since the stage above reached m) and s_min drains
+// up to pair m-mem_limit (then nothing is blocked). Closed form per stage:
+//   n_s = m - dm_s (s > s_min), m - L + 1 - dm_s (s = s_min), 0 (s < s_min).
+// Order within the pass only matters through data dependencies: pair k at
+// stage s needs stage s's previous pair (gpu_free) and the gradient of pair
+// k from stage s+1; each gradient link is written by one stage only. So the
+// pass is evaluated in rounds: round j drains pair dm_s + j at every stage
+// with j < n_s. Inside a round, stage s consumes stage s+1's output of the
+// same round iff dm_s == dm_{s+1} ("linked"); otherwise its input was
+// produced in an earlier round (memory). A round is a max-plus chain down
+// the linked stages: out_s = max(in_s, gf_s) + dur + delta_s + wan_s, with
+// delta_s the exact-fit shift on the stage's WAN gradient link
+// (atlas_pair_start, :287-294). With the deltas fixed it is a composition
+// of maps x -> max(x + a, b), evaluated by one warp suffix scan; the deltas
+// are resolved top-down (the topmost conflicting WAN stage has a final
+// input), rescanning after each, so a round costs 1 + (#shifted WAN stages)
+// scans instead of one sequential step per pair.
+constexpr long long kNegMP = -(1LL << 62);
+
+__device__ __forceinline__ long long mp_add(long long x, long long y) {
+  const long long r = x + y;  // |x|,|y| <= 2^62: no overflow
+  return r < kNegMP ? kNegMP : r;
+}
+
+template <int B, bool TIMELINE>
+__device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L, AtlasMem& X,
+                                              long long (&gfr)[B], int (&drr)[B],
+                                              const int (&wbi)[B], const long long (&serb)[B],
+                                              const long long (&latb)[B], long long& n_pairs,
+                                              long long& n_scans, long long& n_rounds) {
+  const int lane = threadIdx.x & 31;
+  const int S = g.S, M = g.M, C = g.C;
+  const long long dur = g.dur;
+  // lowest blocked stage
+  int my_min = 0x7fffffff;
+#pragma unroll
+  for (int j = B - 1; j >= 0; --j)
+    if (lane * B + j < S && m - drr[j] >= L) my_min = lane * B + j;
+  const int s_min = __reduce_min_sync(kFull, my_min);
+  // pair counts, links (dm of the stage above: next local stage, or lane+1)
+  int cnt[B];
+  bool link[B];
+  const int up_dm = __shfl_down_sync(kFull, drr[0], 1);
+  int nmax = 0;
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    const int s = lane * B + j;
+    cnt[j] = s >= S || s < s_min ? 0 : (s == s_min ? m - L + 1 - drr[j] : m - drr[j]);
+    const int dma = j + 1 < B ? drr[j + 1] : up_dm;
+    link[j] = s + 1 < S && dma == drr[j];
+    nmax = max(nmax, cnt[j]);
+  }
+  const int R = __reduce_max_sync(kFull, nmax);
+  {
+    int tot = 0;
+#pragma unroll
+    for (int j = 0; j < B; ++j) tot += cnt[j];
+    n_pairs += __reduce_add_sync(kFull, tot);
+  }
+  long long wl[B];  // WAN serialization + latency added to the pair's output
+#pragma unroll
+  for (int j = 0; j < B; ++j) wl[j] = wbi[j] >= 0 ? serb[j] + latb[j] : 0;
+
+  n_rounds += R;
+  for (int r = 0; r < R; ++r) {
+    long long xin[B], dl[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const int s = lane * B + j;
+      dl[j] = 0;
+      xin[j] = kNegMP;
+      if (r < cnt[j] && !link[j]) {
+        const int k = drr[j] + r;
+        xin[j] = s == S - 1 ? X.fdl[p * M + k] : X.garr[((size_t)p * S + s) * M + k];
+      }
+    }
+    long long lo[B];
+    for (;;) {
+      ++n_scans;
+      // lane map: stages lane*B+B-1 (applied first) down to lane*B
+      long long ta = 0, tb = kNegMP;
+#pragma unroll
+      for (int j = B - 1; j >= 0; --j) {
+        long long fa = kNegMP, fb = kNegMP;
+        if (r < cnt[j]) {
+          const long long c = dur + dl[j] + wl[j];
+          if (link[j]) {
+            fa = c;
+            fb = gfr[j] + c;
+          } else {
+            fb = imax(xin[j], gfr[j]) + c;
+          }
+        }
+        // (F o T)(x) = max(x + ta + fa, max(tb + fa, fb))
+        ta = mp_add(ta, fa);
+        tb = imax(mp_add(tb, fa), fb);
+      }
+      // inclusive suffix scan over lanes (higher lanes = deeper stages first)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long oa = shfl_down64(ta, o), ob = shfl_down64(tb, o);
+        if (lane + o < 32) {
+          tb = imax(mp_add(ob, ta), tb);
+          ta = mp_add(oa, ta);
+        }
+      }
+      long long v = shfl_down64(tb, 1);  // everything above this lane, at -inf
+      if (lane == 31) v = kNegMP;
+      // evaluate the lane's stages; check the WAN links at their inputs
+      int conf = -1;
+      long long conf_y = 0;
+#pragma unroll
+      for (int j = B - 1; j >= 0; --j) {
+        if (r >= cnt[j]) {
+          v = kNegMP;
+          continue;
+        }
+        lo[j] = imax(link[j] ? v : xin[j], gfr[j]);
+        v = lo[j] + dur + dl[j] + wl[j];
+        const int w = wbi[j];
+        if (w >= 0 && conf < 0) {
+          const long long y = lo[j] + dur + dl[j];
+          LinkCounts kc{X.nm, S, lane * B + j, p, drr[j] + r, 0, M, X.hintb + w * C};
+          if (!union_free_at(X.resb + (size_t)w * C * M, C, M, kc, y, serb[j])) {
+            conf = j;
+            conf_y = y;
+          }
+        }
+      }
+      const unsigned bal = __ballot_sync(kFull, conf >= 0);
+      if (!bal) break;
+      const int src = 31 - __clz(bal);  // topmost conflict: its input is final
+      if (lane == src) {
+        const int w = wbi[conf];
+        LinkCounts kc{X.nm, S, lane * B + conf, p, drr[conf] + r, 0, M, X.hintb + w * C};
+        const long long fit =
+            union_earliest_fit(X.resb + (size_t)w * C * M, C, M, kc, conf_y, serb[conf]);
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+          if (j == conf) dl[j] += fit - conf_y;
+      }
+    }
+    // commit the round
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      if (r >= cnt[j]) continue;
+      const int s = lane * B + j;
+      const int k = drr[j] + r;
+      const long long t = lo[j] + dl[j];
+      const long long e = t + dur;
+      gfr[j] = e;
+      if (wbi[j] >= 0) X.resb[((size_t)wbi[j] * C + p) * M + k] = e;  // reserve
+      if (s > 0) X.garr[((size_t)p * S + s - 1) * M + k] = e + wl[j];
+      if (TIMELINE) X.ps[((size_t)p * S + s) * M + k] = t;
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int j = 0; j < B; ++j) drr[j] += cnt[j];
 }
 
 template <int B, bool TIMELINE>
@@ -234,14 +430,16 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
                                long long* phase = nullptr) {
   const int lane = threadIdx.x & 31;
   long long ph_casc = 0, ph_chain = 0, ph_fit = 0, ph_drain = 0, ph_t = 0;
-  long long n_stage_it = 0, n_pairs = 0, n_adm = 0;
+  long long n_stage_it = 0, n_pairs = 0, n_adm = 0, n_rounds = 0;
   const int S = g.S, M = g.M, C = g.C;
   const long long f = g.fwd, dur = g.dur;
   const int nw = g.nb - 1;
+  X.garr = (long long)C * S * M <= X.garr_cap ? X.garr_smem : X.garr_glob;
   for (int i = lane; i < C * S; i += 32) {
     X.gf[i] = 0;
     X.nm[i] = 0;
   }
+  for (int i = lane; i < nw * C; i += 32) X.hintf[i] = X.hintb[i] = 0;
   for (int s = lane; s < S; s += 32) {
     int w;
     X.wbs[s] = (s > 0 && wan_after(g, s - 1, w)) ? w : -1;
@@ -305,94 +503,11 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
       for (int j = 0; j < B; ++j)
         if (lane * B + j < S && m - drr[j] >= mem_limit) ++nblk;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) nblk += __shfl_xor_sync(kFull, nblk, o);
+      nblk = __reduce_add_sync(kFull, nblk);
       if (nblk > 0) {
-        // The cascade is one descending pass over the stages; it runs in
-        // lane 0 on shared copies of this pipeline's state, forwarding the
-        // gradient just produced by the stage above in a register.
-#pragma unroll
-        for (int j = 0; j < B; ++j) {
-          const int s = lane * B + j;
-          if (s < S) {
-            X.gf[p * S + s] = gfr[j];
-            X.nm[p * S + s] = drr[j];
-          }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          long long* __restrict__ gfp = X.gf + p * S;
-          int* __restrict__ nmp = X.nm + p * S;
-          long long* __restrict__ garr = X.garr;
-          const long long* __restrict__ fdl = X.fdl + p * M;
-          int nb = nblk, up = m, carry_m = -1;
-          long long carry = 0;
-          // software-pipelined: stage s-1's state is loaded while s drains
-          int n_dm = nmp[S - 1], n_w = X.wbs[S - 1];
-          long long n_gf = gfp[S - 1];
-          for (int s = S - 1; s >= 0 && nb > 0; --s) {
-            int dm = n_dm;
-            const int w = n_w;
-            long long gfi = n_gf;
-            if (s > 0) {
-              n_dm = nmp[s - 1];
-              n_w = X.wbs[s - 1];
-              n_gf = gfp[s - 1];
-            }
-            const int u = up;
-            up = dm;
-            ++n_stage_it;
-            if (dm >= M || dm >= u) {  // no ready pair: nothing new for s-1
-              carry_m = -1;
-              continue;
-            }
-            const long long ser = w >= 0 ? X.wa[8 + w] : 0;  // boundary constants
-            const long long lat = w >= 0 ? X.wg[8 + w] : 0;
-            long long produced = 0;
-            int pm = -1;
-            while (dm < M && dm < u && nb > 0) {
-              const long long ready =
-                  s == S - 1 ? fdl[dm]
-                             : (dm == carry_m ? carry : garr[((size_t)p * S + s) * M + dm]);
-              const long long lo = imax(ready, gfi);
-              long long t = lo;
-              if (w >= 0) {
-                long long* base = X.resb + (size_t)w * C * M;
-                LinkCounts k{X.nm, S, s, p, dm, 0, M};
-                t = union_earliest_fit(base, C, M, k, lo + dur, ser) - dur;
-                base[(size_t)p * M + dm] = t + dur;  // reserve (append to list p)
-              }
-              const long long e = t + dur;  // atlas_commit_pair (:298-317)
-              gfi = imax(gfi, e);
-              produced = w >= 0 ? e + ser + lat : e;
-              pm = dm;
-              if (s > 0) garr[((size_t)p * S + s - 1) * M + dm] = produced;
-              if (TIMELINE) X.ps[((size_t)p * S + s) * M + dm] = t;
-              if (m - dm >= mem_limit && m - (dm + 1) < mem_limit) --nb;
-              ++dm;
-              ++n_pairs;
-            }
-            gfp[s] = gfi;
-            nmp[s] = dm;
-            up = dm;
-            carry = produced;
-            carry_m = pm;
-          }
-          X.done[0] = nb;  // > 0: DeadlockError (unreachable)
-          ++n_adm;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < B; ++j) {
-          const int s = lane * B + j;
-          if (s < S) {
-            gfr[j] = X.gf[p * S + s];
-            drr[j] = X.nm[p * S + s];
-          }
-        }
-        if (X.done[0] > 0) {
-          err = 1;
-          return 0;
-        }
+        atlas_cascade<B, TIMELINE>(g, p, m, mem_limit, X, gfr, drr, wbi, serb, latb, n_pairs,
+                                   n_stage_it, n_rounds);
+        ++n_adm;
       }
       if (phase) {
         const long long t1 = clock64();
@@ -437,6 +552,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
       {
         LinkCounts k{nullptr, S, 0, p, m, 1, M};
         for (int w = 0; w < nw;) {
+          k.hint = X.hintf + w * C;
           const long long e = X.wa[w] + f + imax(t0, X.wg[w]);
           const long long* base = X.resf + (size_t)w * C * M;
           const long long len = g.ser_pooled[w];
@@ -589,6 +705,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     phase[4] = n_stage_it;
     phase[5] = n_pairs;
     phase[6] = n_adm;
+    phase[7] = n_rounds;
   }
   // -------------------------------------------- right-pack (timeline)
   if (TIMELINE) {
@@ -629,7 +746,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
 }
 
 template <int B>
-__global__ void __launch_bounds__(kEvalThreads) atlas_kernel(EvalArgs a) {
+__global__ void __launch_bounds__(kEvalThreads, 1) atlas_kernel(EvalArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -654,7 +771,7 @@ __global__ void __launch_bounds__(kEvalThreads) atlas_kernel(EvalArgs a) {
 }
 
 template <int B>
-__global__ void __launch_bounds__(kEvalThreads) atlas_timeline_kernel(EvalArgs a) {
+__global__ void __launch_bounds__(kEvalThreads, 1) atlas_timeline_kernel(EvalArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -711,6 +828,29 @@ static cudaError_t launch_atlas_b(const EvalArgs& a, int grid, int wpc, cudaStre
   if (e != cudaSuccess) return e;
   atlas_kernel<B><<<grid, 32 * wpc, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+// Resident blocks per SM of the ATLAS kernel (registers + shared memory).
+int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem) {
+  int n = 0;
+  cudaError_t e = cudaSuccess;
+#define GPB_OCC(BB)                                                                         \
+  case BB:                                                                                  \
+    e = timeline ? cudaFuncSetAttribute(atlas_timeline_kernel<BB>,                          \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) \
+                 : cudaFuncSetAttribute(atlas_kernel<BB>,                                   \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e == cudaSuccess)                                                                   \
+      e = timeline ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_timeline_kernel<BB>, \
+                                                                   32 * wpc, smem)          \
+                   : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_kernel<BB>,    \
+                                                                   32 * wpc, smem);         \
+    break;
+  switch (B) {
+    GPB_OCC(1) GPB_OCC(2) GPB_OCC(3) GPB_OCC(4) GPB_OCC(5) GPB_OCC(6) GPB_OCC(7) GPB_OCC(8)
+  }
+#undef GPB_OCC
+  return e == cudaSuccess ? n : 0;
 }
 
 cudaError_t launch_atlas(int B, const EvalArgs& a, int grid, int wpc, cudaStream_t st) {

@@ -81,6 +81,8 @@ def load_library(path: str = LIB_PATH):
         "gpb_timeline_arrays": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_int64), P(C.c_int64),
                                           C.c_int64, P(C.c_int32), P(C.c_int64)]),
         "gpb_fetch_row_cycles": (C.c_int, [C.c_void_p, P(C.c_int64), C.c_int64]),
+        "gpb_bucket_infos": (C.c_int, [C.c_void_p, P(abi.BucketInfo), C.c_int32,
+                                       P(C.c_int32)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -96,7 +98,7 @@ def exported_symbols():
             "gpb_fetch_best", "gpb_device_best", "gpb_bubbles", "gpb_pack_prefills",
             "gpb_synthetic_requests", "gpb_get_timing", "gpb_microbench", "gpb_set_stream",
             "gpb_copy_best", "gpb_set_profile", "gpb_fetch_row_cycles",
-            "gpb_set_allreduce_tail", "gpb_timeline_arrays"]
+            "gpb_set_allreduce_tail", "gpb_timeline_arrays", "gpb_bucket_infos"]
 
 
 @dataclass
@@ -196,6 +198,14 @@ class Planner:
         t = abi.Timing()
         self._check(self.lib.gpb_get_timing(self.ctx, C.byref(t)))
         return t
+
+    def bucket_infos(self):
+        """Per-bucket shapes and device times of the last evaluate()."""
+        n = C.c_int32()
+        self._check(self.lib.gpb_bucket_infos(self.ctx, None, 0, C.byref(n)))
+        out = (abi.BucketInfo * max(1, n.value))()
+        self._check(self.lib.gpb_bucket_infos(self.ctx, out, n.value, C.byref(n)))
+        return list(out[: n.value])
 
     def microbench(self, kind: int = 0) -> float:
         g = C.c_double()

@@ -1,0 +1,44 @@
+"""GPU parity at BASELINE config 2's full size (the bench workload): every one
+of the 10^4 (scenario, D) rows of the Llama-3 70B plan search, all four
+policies, bit-exact against the reference's select() (oracle/_ref compiled
+from the reference sources, else the C port), plus the per-scenario choice
+and the global best. The reference runs on a host thread pool (its core is
+re-entrant)."""
+from concurrent.futures import ThreadPoolExecutor
+import os
+
+import pytest
+
+from paper_2411_14458_b200 import abi, workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def _key(r):
+    return (r.d, r.feasible, r.chosen, r.pp_time_ms, r.allreduce_time_ms, r.total_time_ms,
+            r.throughput, tuple(r.partitions))
+
+
+def test_config2_all_rows_bit_exact(planner, checker):
+    topos, scens = workloads.config2(10_000, seed=1)
+    tarr = abi.array(abi.Topology, topos)
+    n = planner.load(tarr, abi.array(abi.Scenario, scens))
+    assert n == 10_000
+    planner.evaluate()
+    rows = planner.rows()
+    res = planner.scenario_results()
+    order = sorted(range(len(scens)), key=lambda i: -scens[i].num_microbatches * scens[i].d_max)
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        ref = dict(zip(order, ex.map(lambda i: checker.select(tarr, scens[i]), order)))
+    best = (-1.0, -1)
+    for i, sc in enumerate(scens):
+        ref_rows, chosen, used = ref[i]
+        r0 = res[i].first_row
+        assert (res[i].n_rows, res[i].chosen_d, res[i].gpus_used) == (len(ref_rows), chosen, used)
+        for k, b in enumerate(ref_rows):
+            a = rows[r0 + k]
+            assert _key(a) == _key(b), (i, k + 1, abi.POLICY_NAMES[sc.policy], _key(a), _key(b))
+            if b.feasible == 1 and b.throughput > best[0]:
+                best = (b.throughput, r0 + k)
+    got = planner.best()
+    assert (got.throughput, got.row) == best

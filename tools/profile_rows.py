@@ -38,6 +38,6 @@ tot = sum(v[1] for v in agg.values())
 print(json.dumps({"evaluate_ms": t.evaluate_ms, "policy_ms": list(t.policy_ms)}))
 print("policy S C M feas | rows  sum_Mcyc  share  max_kcyc")
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:25]:
-    ph = [round(x / max(1, v[1]) * 100) for x in v[3][:4]] + [round(x / v[0]) for x in v[3][4:7]]
+    ph = [round(x / max(1, v[1]) * 100) for x in v[3][:4]] + [round(x / v[0]) for x in v[3][4:8]]
     print(*k, "|", v[0], round(v[1] / 1e6, 2), f"{100 * v[1] / tot:.1f}%", round(v[2] / 1e3, 1),
-          "phases% casc/chain/fit/drain + per-row stage_it/pairs/adm", ph)
+          "phases% casc/chain/fit/drain + per-row scans/pairs/adm/rounds", ph)
