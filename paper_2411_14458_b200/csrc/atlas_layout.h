@@ -16,7 +16,7 @@ struct AtlasLayout {
   // outputs
   size_t off_wa, off_wg, off_wbs, off_gf, off_cand, off_lastc, off_nm, off_done,
       off_firstm, off_pub_nm, off_pub_last, off_pub_done, off_fdl, off_resf, off_resb,
-      off_hint, off_garr, total;
+      off_hint, off_mf, off_mb, off_mtmp, off_mcnt, off_garr, total;
   int cap;             // list storage per WAN boundary = C * M (C lists of M)
 
   __host__ __device__ static size_t al(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -41,6 +41,11 @@ struct AtlasLayout {
     off_resf = o;      o = al(o + (size_t)nw * cap * 8);
     off_resb = o;      o = al(o + (size_t)nw * cap * 8);
     off_hint = o;      o = al(o + (size_t)2 * (nw > 0 ? nw : 1) * C * 4);  // search cursors
+    // merged static lists (pipelines < p) per WAN link, forward / gradient
+    off_mf = o;        o = al(o + (size_t)nw * cap * 8);
+    off_mb = o;        o = al(o + (size_t)nw * cap * 8);
+    off_mtmp = o;      o = al(o + (size_t)cap * 8);
+    off_mcnt = o;      o = al(o + 32 * 4);                // counts / cursors
     off_garr = o;
     o = al(o + (size_t)garr_cap * 8);
     total = o;

@@ -215,6 +215,8 @@ struct AtlasMem {
   long long *garr_smem, *garr_glob;
   long long garr_cap;
   int *wbs, *nm, *done, *firstm, *pub_nm, *pub_done, *hintf, *hintb;
+  long long *mf, *mb, *mtmp;  // merged static link lists (forward phase)
+  int* mcnt;                  // [w] |mf|, [8+w] |mb|, [16+w] mb cursor
   long long* fe;  // timeline: forward ends [C][S][M] (global)
   long long* ps;  // timeline: pair starts  [C][S][M] (global)
 
@@ -236,6 +238,10 @@ struct AtlasMem {
     resb = (long long*)(base + L.off_resb);
     hintf = (int*)(base + L.off_hint);
     hintb = hintf + (L.nw > 0 ? L.nw : 1) * L.C;
+    mf = (long long*)(base + L.off_mf);
+    mb = (long long*)(base + L.off_mb);
+    mtmp = (long long*)(base + L.off_mtmp);
+    mcnt = (int*)(base + L.off_mcnt);
     garr_smem = (long long*)(base + L.off_garr);
     garr_glob = garr_global;
     garr_cap = L.garr_cap;
@@ -254,6 +260,69 @@ __device__ __forceinline__ long long atlas_cand(const Geom& g, const AtlasMem& X
   if (wb < 0) return lo;
   LinkCounts k{X.nm, S, s, -1, 0, 0, M, X.hintb + wb * C};
   return union_earliest_fit(X.resb + (size_t)wb * C * M, C, M, k, lo + g.dur, serb) - g.dur;
+}
+
+// ------------------------------------------- forward-phase link lists
+//
+// While pipeline p runs its forward phase (chains + memory-cap drains), every
+// other pipeline's reservations on every link are fixed: pipelines q < p are
+// finished (their remaining pairs drain after all forwards) and q > p have
+// none. So each link is one static sorted list — the merge of pipelines
+// 0..p-1, rebuilt when p starts — plus p's own append-only list. Queries on a
+// link during p's phase come in non-decreasing time order and always start
+// after p's own last reservation (gpu_free grows), so only the own tail can
+// overlap: a monotone cursor over the static list plus one comparison with
+// the own tail answer free_at / earliest_fit (base.h:65-84) exactly.
+
+// first index >= i0 with v[i] >= x (v sorted), by bisection
+__device__ __forceinline__ int lower_idx(const long long* v, int n, long long x, bool upper) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (upper ? v[mid] <= x : v[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// A[0..na) <- merge(A, Bv[0..nb)) through tmp (warp-parallel merge path:
+// every element lands at its index plus its rank in the other list; A wins
+// ties).
+__device__ __forceinline__ void warp_merge(long long* A, int na, const long long* Bv, int nb,
+                                           long long* tmp) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < na; i += 32) tmp[i + lower_idx(Bv, nb, A[i], false)] = A[i];
+  for (int j = lane; j < nb; j += 32) tmp[j + lower_idx(A, na, Bv[j], true)] = Bv[j];
+  __syncwarp();
+  for (int i = lane; i < na + nb; i += 32) A[i] = tmp[i];
+  __syncwarp();
+}
+
+// [x, x+len) overlaps a static entry (cursor `cur`, advanced) or the own tail
+__device__ __forceinline__ bool link_conflict(const long long* mg, int n, int& cur,
+                                              long long own_last, long long len, long long x) {
+  if (len <= 0) return false;
+  while (cur < n && mg[cur] + len <= x) ++cur;
+  if (cur < n && mg[cur] < x + len) return true;
+  return own_last + len > x;
+}
+
+// earliest_fit over the static list and the own tail
+__device__ __forceinline__ long long link_fit(const long long* mg, int n, int& cur,
+                                              long long own_last, long long len, long long x) {
+  if (len <= 0) return x;
+  long long t = x;
+  for (;;) {
+    while (cur < n && mg[cur] + len <= t) ++cur;
+    if (cur < n && mg[cur] < t + len) {
+      t = mg[cur] + len;
+      continue;
+    }
+    if (own_last + len > t) {
+      t = own_last + len;
+      continue;
+    }
+    return t;
+  }
 }
 
 // ------------------------------------------------ admission cascade
@@ -386,8 +455,10 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
         const int w = wbi[j];
         if (w >= 0 && conf < 0) {
           const long long y = lo[j] + dur + dl[j];
-          LinkCounts kc{X.nm, S, lane * B + j, p, drr[j] + r, 0, M, X.hintb + w * C};
-          if (!union_free_at(X.resb + (size_t)w * C * M, C, M, kc, y, serb[j])) {
+          const int k = drr[j] + r;
+          const long long own = k > 0 ? X.resb[((size_t)w * C + p) * M + k - 1] : kNegMP;
+          if (link_conflict(X.mb + (size_t)w * C * M, X.mcnt[8 + w], X.mcnt[16 + w], own,
+                            serb[j], y)) {
             conf = j;
             conf_y = y;
           }
@@ -398,9 +469,10 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
       const int src = 31 - __clz(bal);  // topmost conflict: its input is final
       if (lane == src) {
         const int w = wbi[conf];
-        LinkCounts kc{X.nm, S, lane * B + conf, p, drr[conf] + r, 0, M, X.hintb + w * C};
-        const long long fit =
-            union_earliest_fit(X.resb + (size_t)w * C * M, C, M, kc, conf_y, serb[conf]);
+        const int k = drr[conf] + r;
+        const long long own = k > 0 ? X.resb[((size_t)w * C + p) * M + k - 1] : kNegMP;
+        const long long fit = link_fit(X.mb + (size_t)w * C * M, X.mcnt[8 + w], X.mcnt[16 + w],
+                                       own, serb[conf], conf_y);
 #pragma unroll
         for (int j = 0; j < B; ++j)
           if (j == conf) dl[j] += fit - conf_y;
@@ -489,12 +561,33 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
   // counts of the owned stages (written back to shared memory per p).
   long long gfr[B];
   int drr[B];
+  if (lane < 8) X.mcnt[lane] = X.mcnt[8 + lane] = 0;
+  __syncwarp();
+  int curf = 0;  // lane w: cursor of the static forward list of link w
   for (int p = 0; p < C; ++p) {
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       gfr[j] = 0;
       drr[j] = 0;
     }
+    if (p > 0) {  // fold pipeline p-1 into the static lists of every link
+      for (int w = 0; w < nw; ++w) {
+        const int sw = g.blk_first[w + 1];  // stage whose gradient link is w
+        const int nf = X.mcnt[w], nbk = X.mcnt[8 + w];
+        const int add_b = X.nm[(p - 1) * S + sw];
+        warp_merge(X.mf + (size_t)w * C * M, nf, X.resf + ((size_t)w * C + p - 1) * M, M, X.mtmp);
+        warp_merge(X.mb + (size_t)w * C * M, nbk, X.resb + ((size_t)w * C + p - 1) * M, add_b,
+                   X.mtmp);
+        if (lane == 0) {
+          X.mcnt[w] = nf + M;
+          X.mcnt[8 + w] = nbk + add_b;
+        }
+        __syncwarp();
+      }
+    }
+    if (lane < 8) X.mcnt[16 + lane] = 0;
+    curf = 0;
+    __syncwarp();
     for (int m = 0; m < M; ++m) {
       // memory-cap admission (:366-381) + forced drains (:321-346)
       if (phase) ph_t = clock64();
@@ -549,22 +642,31 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
       }
       // exact-fit shift loop over the WAN boundaries (:383-405), one lane per
       // pipeline list of each link, then the chain's reservations (:407-430)
-      {
-        LinkCounts k{nullptr, S, 0, p, m, 1, M};
-        for (int w = 0; w < nw;) {
-          k.hint = X.hintf + w * C;
-          const long long e = X.wa[w] + f + imax(t0, X.wg[w]);
-          const long long* base = X.resf + (size_t)w * C * M;
-          const long long len = g.ser_pooled[w];
-          if (!warp_union_free_at(base, C, M, k, e, len)) {
-            t0 += warp_union_earliest_fit(base, C, M, k, e, len) - e;
-            w = 0;  // restart the chain
-          } else {
-            ++w;
-          }
+      // (lane w checks link w; the lowest conflicting link shifts t0, as the
+      // reference's restart from stage 0 does)
+      if (nw > 0) {
+        long long aw = 0, gw = 0, lenw = 0, ownw = kNegMP;
+        const long long* mgw = nullptr;
+        int nmw = 0;
+        if (lane < nw) {
+          aw = X.wa[lane];
+          gw = X.wg[lane];
+          lenw = X.wa[8 + lane];
+          mgw = X.mf + (size_t)lane * C * M;
+          nmw = X.mcnt[lane];
+          if (m > 0) ownw = X.resf[((size_t)lane * C + p) * M + m - 1];
         }
-        if (lane < nw)
-          X.resf[((size_t)lane * C + p) * M + m] = X.wa[lane] + f + imax(t0, X.wg[lane]);
+        for (;;) {
+          const long long e = aw + f + imax(t0, gw);
+          const bool conf = lane < nw && link_conflict(mgw, nmw, curf, ownw, lenw, e);
+          const unsigned bal = __ballot_sync(kFull, conf);
+          if (!bal) break;
+          const int src = __ffs(bal) - 1;
+          long long shift = 0;
+          if (lane == src) shift = link_fit(mgw, nmw, curf, ownw, lenw, e) - e;
+          t0 += shfl_idx64(shift, src);
+        }
+        if (lane < nw) X.resf[((size_t)lane * C + p) * M + m] = aw + f + imax(t0, gw);
       }
       if (phase) {
         const long long t1 = clock64();
