@@ -293,6 +293,10 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
                               (d.recompute ? (long long)std::llround(d.rec_ms * 1e6) : 0);
         if (dur <= 0)
           throw ConfigErr{P_(i) + ": atlas pair duration rounds to 0 ns (outside the envelope)"};
+        // one lane per pipeline in the per-stage drain greedy
+        if (d.C > 32)
+          throw ConfigErr{P_(i) + ": atlas with more than 32 pipelines per cell is outside the "
+                                  "kernel envelope"};
       }
       int order[GPB_MAX_DC];
       int n_order = s.n_order;

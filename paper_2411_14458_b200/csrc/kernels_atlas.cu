@@ -497,6 +497,162 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
   for (int j = 0; j < B; ++j) drr[j] += cnt[j];
 }
 
+// --------------------------------------------------------- drain phase
+//
+// The reference's drain (scheduler.cpp:461-505) is a global greedy over all
+// (pipeline, stage) next pairs. Stage s reads only its own GPUs, its own
+// gradient link (boundary s-1) and the gradient arrivals of stage s+1, and
+// the greedy commits in non-decreasing start time; a pair that is not ready
+// yet becomes ready only after its producer commits, strictly later (pair
+// duration > 0). So the global greedy equals, stage by stage from S-1 down,
+// a per-stage greedy with every input of the stage known:
+//  * a stage without a WAN gradient link has no shared resource: pipeline
+//    p's pairs follow e[m] = max(r[m], e[m-1]) + dur, i.e.
+//    e[m] = (m+1)*dur + max(gf0 - m0*dur, max_{m0<=j<=m} (r[j] - j*dur)),
+//    one segmented prefix-max over the stage's (pipeline, microbatch) pairs;
+//  * a stage with a WAN gradient link runs the greedy over its C pipelines
+//    (lane = pipeline, warp argmin, lowest pipeline on ties). Its link holds
+//    the forward phase's forced drains (a static merged list) plus this
+//    stage's commits, which come in non-decreasing time; every later query
+//    starts at or after the last commit, so only that one can overlap.
+
+// Stage s without a WAN gradient link: segmented prefix max, K pairs per lane.
+template <bool TIMELINE>
+__device__ void drain_stage_scan(const Geom& g, AtlasMem& X, int s) {
+  constexpr int K = 8;
+  const int lane = threadIdx.x & 31;
+  const int S = g.S, M = g.M, C = g.C;
+  const long long dur = g.dur;
+  const long long n = (long long)C * M;
+  long long carry = kNegMP;
+  for (long long base = 0; base < n; base += 32 * K) {
+    const long long rem = n - base < 32 * K ? n - base : 32 * K;
+    const int kk = (int)((rem + 31) / 32);
+    long long u[K];
+    bool rs[K], act[K];
+    int rs_first = K;
+    long long acc = kNegMP;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      u[i] = kNegMP;
+      rs[i] = act[i] = false;
+      const long long idx = base + (long long)lane * kk + i;
+      if (i < kk && idx < base + rem) {
+        const int p = (int)(idx / M), m = (int)(idx - (long long)p * M);
+        const int m0 = X.nm[p * S + s];
+        if (m >= m0) {
+          act[i] = true;
+          const long long r = s == S - 1 ? X.fdl[p * M + m] : X.garr[((size_t)p * S + s) * M + m];
+          long long v = r - (long long)m * dur;
+          if (m == m0) {
+            rs[i] = true;
+            v = imax(v, X.gf[p * S + s] - (long long)m0 * dur);
+          }
+          u[i] = v;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) {  // lane-local inclusive segmented max
+      if (rs[i]) {
+        acc = u[i];
+        if (rs_first == K) rs_first = i;
+      } else {
+        acc = imax(acc, u[i]);
+      }
+      u[i] = acc;
+    }
+    // warp inclusive segmented scan of the lane aggregates
+    bool f = rs_first < K;
+    long long a = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long oa = shfl_up64(a, o);
+      const bool of = __shfl_up_sync(kFull, (int)f, o) != 0;
+      if (lane >= o) {
+        if (!f) a = imax(a, oa);
+        f = f || of;
+      }
+    }
+    long long ex = shfl_up64(a, 1);
+    bool exf = __shfl_up_sync(kFull, (int)f, 1) != 0;
+    if (lane == 0) {
+      ex = kNegMP;
+      exf = false;
+    }
+    const long long pre = exf ? ex : imax(carry, ex);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (!act[i]) continue;
+      const long long idx = base + (long long)lane * kk + i;
+      const int p = (int)(idx / M), m = (int)(idx - (long long)p * M);
+      const long long uu = i >= rs_first ? u[i] : imax(pre, u[i]);
+      const long long e = (long long)(m + 1) * dur + uu;
+      if (s > 0) X.garr[((size_t)p * S + s - 1) * M + m] = e;
+      if (TIMELINE) X.ps[((size_t)p * S + s) * M + m] = e - dur;
+      if (m == M - 1) X.gf[p * S + s] = e;
+    }
+    const long long tot = f ? a : imax(carry, a);
+    carry = shfl_idx64(tot, 31);
+  }
+  __syncwarp();
+  for (int p = lane; p < C; p += 32) X.nm[p * S + s] = M;
+  __syncwarp();
+}
+
+// Stage s whose gradient link w crosses the WAN: per-stage greedy, lane q =
+// pipeline q (C <= 32, host-checked).
+template <bool TIMELINE>
+__device__ void drain_stage_greedy(const Geom& g, AtlasMem& X, int s, int w) {
+  const int q = threadIdx.x & 31;
+  const int S = g.S, M = g.M, C = g.C;
+  const long long dur = g.dur, len = g.ser_pooled[w], wl = g.ser_pooled[w] + g.lat[w];
+  const long long* mg = X.mb + (size_t)w * C * M;
+  const int nmg = X.mcnt[8 + w];
+  int mq = q < C ? X.nm[q * S + s] : M;
+  long long gfq = q < C ? X.gf[q * S + s] : 0;
+  int cur = 0;
+  long long last_a = kNegMP;  // start of this stage's last committed transfer
+  auto fresh = [&]() -> long long {
+    const long long r = s == S - 1 ? X.fdl[q * M + mq] : X.garr[((size_t)q * S + s) * M + mq];
+    return link_fit(mg, nmg, cur, last_a, len, imax(r, gfq) + dur) - dur;
+  };
+  long long cand = mq < M ? fresh() : kInf64;
+  for (;;) {
+    long long b = cand;
+    int bq = q;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const long long ob = __shfl_xor_sync(kFull, b, o);
+      const int oq = __shfl_xor_sync(kFull, bq, o);
+      if (ob < b || (ob == b && oq < bq)) {
+        b = ob;
+        bq = oq;
+      }
+    }
+    if (b == kInf64) break;
+    if (q == bq) {  // atlas_commit_pair (:298-317) + reserve
+      const long long e = b + dur;
+      X.resb[((size_t)w * C + q) * M + mq] = e;
+      X.garr[((size_t)q * S + s - 1) * M + mq] = e + wl;
+      if (TIMELINE) X.ps[((size_t)q * S + s) * M + mq] = b;
+      gfq = e;
+      ++mq;
+    }
+    last_a = b + dur;
+    if (q == bq) {
+      cand = mq < M ? fresh() : kInf64;
+    } else if (cand != kInf64 && cand + dur < last_a + len) {
+      cand = link_fit(mg, nmg, cur, last_a, len, cand + dur) - dur;  // pushed by the commit
+    }
+  }
+  if (q < C) {
+    X.gf[q * S + s] = gfq;
+    X.nm[q * S + s] = M;
+  }
+  __syncwarp();
+}
+
 template <int B, bool TIMELINE>
 __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& err,
                                long long* phase = nullptr) {
@@ -697,107 +853,26 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
   }
 
   if (phase) ph_t = clock64();
-  // ------------------------------------------ drain: per-stage wavefront
-#pragma unroll
-  for (int j = 0; j < B; ++j) {
-    const int s = lane * B + j;
-    if (s < S) {
-      X.lastc[s] = -kInf64;
-      int all = 1;
-      for (int p = 0; p < C; ++p) {
-        const int i = p * S + s;
-        const int m = X.nm[i];
-        X.firstm[i] = m;
-        all &= m >= M;
-        const bool ready = m < M && (s == S - 1 || X.nm[i + 1] > m);
-        X.cand[i] = ready ? atlas_cand(g, X, p, s, m, wbi[j], serb[j]) : kInf64;
-      }
-      X.done[s] = all;
-    }
+  // ------------------------------------------ drain: stage by stage
+  // Pairs drained by the forward phase are excluded from the right-pack.
+  for (int i = lane; i < C * S; i += 32) X.firstm[i] = X.nm[i];
+  // the last pipeline's forced drains join the static gradient lists
+  for (int w = 0; w < nw; ++w) {
+    const int sw = g.blk_first[w + 1];
+    const int nbk = X.mcnt[8 + w], add_b = X.nm[(C - 1) * S + sw];
+    warp_merge(X.mb + (size_t)w * C * M, nbk, X.resb + ((size_t)w * C + C - 1) * M, add_b,
+               X.mtmp);
+    if (lane == 0) X.mcnt[8 + w] = nbk + add_b;
+    __syncwarp();
   }
-  __syncwarp();
-  auto publish = [&]() {
-    const int s0 = lane * B;
-    if (s0 < S) {
-      for (int p = 0; p < C; ++p) X.pub_nm[p * 32 + lane] = X.nm[p * S + s0];
-      X.pub_last[lane] = X.lastc[s0];
-      X.pub_done[lane] = X.done[s0];
+  for (int s = S - 1; s >= 0; --s) {
+    const int w = X.wbs[s];
+    if (w < 0) {
+      drain_stage_scan<TIMELINE>(g, X, s);
     } else {
-      X.pub_done[lane] = 1;
+      drain_stage_greedy<TIMELINE>(g, X, s, w);
     }
-  };
-  publish();
-  __syncwarp();
-  for (;;) {
-    bool active = false;
-#pragma unroll
-    for (int j = 0; j < B; ++j) {
-      const int s = lane * B + j;
-      if (s < S && !X.done[s]) active = true;
-    }
-    if (!__any_sync(kFull, active)) break;
-#pragma unroll
-    for (int j = B - 1; j >= 0; --j) {
-      const int s = lane * B + j;
-      if (s >= S || X.done[s]) continue;
-      const bool up = s + 1 < S;
-      const bool up_pub = up && j == B - 1;  // stage s+1 lives in lane+1
-      int up_done = 1;
-      long long up_last = kInf64;
-      if (up) {
-        up_done = up_pub ? X.pub_done[lane + 1] : X.done[s + 1];
-        up_last = up_pub ? X.pub_last[lane + 1] : X.lastc[s + 1];
-      }
-      for (int p = 0; p < C; ++p) {  // gradients that arrived since last round
-        const int i = p * S + s;
-        const int m = X.nm[i];
-        if (m < M && X.cand[i] == kInf64) {
-          const int un = !up ? M : (up_pub ? X.pub_nm[p * 32 + lane + 1] : X.nm[i + 1]);
-          if (un > m) X.cand[i] = atlas_cand(g, X, p, s, m, wbi[j], serb[j]);
-        }
-      }
-      const long long bound =
-          (!up || up_done) ? kInf64 : (up_last == -kInf64 ? -kInf64 : up_last + dur);
-      for (int q = 0; q < kAtlasQ; ++q) {
-        long long bt = kInf64;
-        int bp = -1;
-        for (int p = 0; p < C; ++p) {
-          const long long t = X.cand[p * S + s];
-          if (t < bt) {  // strict: lowest p wins ties (scan order p asc)
-            bt = t;
-            bp = p;
-          }
-        }
-        if (bp < 0 || bt >= bound) break;
-        const int i = bp * S + s;
-        const int m = X.nm[i];
-        const int w = wbi[j];
-        if (w >= 0) X.resb[((size_t)w * C + bp) * M + m] = bt + dur;  // reserve
-        X.gf[i] = bt + dur;
-        if (s > 0)
-          X.garr[((size_t)bp * S + s - 1) * M + m] =
-              w >= 0 ? bt + dur + serb[j] + latb[j] : bt + dur;
-        if (TIMELINE) X.ps[((size_t)bp * S + s) * M + m] = bt;
-        X.nm[i] = m + 1;
-        X.lastc[s] = bt;
-        // refresh: every pipeline of the stage when the gradient link is
-        // shared (the new reservation may push them), else only bp
-        for (int p = w >= 0 ? 0 : bp; p < (w >= 0 ? C : bp + 1); ++p) {
-          const int i2 = p * S + s;
-          const int m2 = X.nm[i2];
-          const int un = !up ? M : (up_pub ? X.pub_nm[p * 32 + lane + 1] : X.nm[i2 + 1]);
-          X.cand[i2] = (m2 < M && un > m2) ? atlas_cand(g, X, p, s, m2, w, serb[j]) : kInf64;
-        }
-      }
-      int all = 1;
-      for (int p = 0; p < C; ++p) all &= X.nm[p * S + s] >= M;
-      X.done[s] = all;
-    }
-    __syncwarp();
-    publish();
-    __syncwarp();
   }
-
   if (phase && lane == 0) {
     ph_drain = clock64() - ph_t;
     phase[0] = ph_casc;
