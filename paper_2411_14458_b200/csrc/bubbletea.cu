@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -167,6 +169,7 @@ struct PackArgs {
   const long long* hz;
   const gpb_request* reqs;
   long long n_req;
+  const long long* sufmin;  // [r] = min arrival (ns) of requests r.. (caps stay valid)
   long long first_late_req_dummy;
   // prefill model (PrefillModel, bubbletea.h:38-58), pre-validated
   double sat_ms, stage_bw, lat_ms;
@@ -178,6 +181,10 @@ struct PackArgs {
   long long* pool_hi;
   unsigned char* pool_fl;
   long long pool_per_slot;
+  int max_pipes;              // largest C*S over the slots (shared-memory caps)
+  long long* stats;           // nullable: per-slot counters (GPB_PACK_STATS)
+  unsigned* memo;             // [slot][pipeline][token bit]: search failed for all later arrivals
+  int memo_words;             // 32-bit words per pipeline = ceil(max_tokens / 32)
   long long* gpu_off;       // [slot gpu base + gi]  -1 = shared
   int* gpu_cnt;
   int* gpu_cap;
@@ -251,6 +258,47 @@ __device__ __forceinline__ long long next_start(const ListView& v, long long x, 
   return kInf64;
 }
 
+// last_start_le from a cursor c <= the answer (queries inside one search are
+// non-decreasing): gallop forward, then bisect; c < -1 means unknown.
+__device__ __forceinline__ int last_start_le_from(const ListView& v, long long x, int& c) {
+  int j;
+  if (c < -1) {
+    j = last_start_le(v, x);
+  } else {
+    j = c;
+    int step = 1;
+    while (j + step < v.n && v.lo[j + step] <= x) {
+      j += step;
+      step <<= 1;
+    }
+    int lo = j + 1, hi = min(j + step, v.n);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (v.lo[mid] <= x) lo = mid + 1; else hi = mid;
+    }
+    j = lo - 1;
+  }
+  c = j;
+  return j;
+}
+
+// fitting_gap / next_start given j = last_start_le(v, x)
+__device__ __forceinline__ bool fits_at(const ListView& v, int j, long long lo, long long dur,
+                                        long long guard) {
+  if (j < 0) return false;
+  if (lo + dur <= usable_end(v, j, guard)) return true;
+  return dur == 0 && j >= 1 && v.hi[j - 1] == lo && usable_end(v, j - 1, guard) >= lo;
+}
+__device__ __forceinline__ long long next_start_from(const ListView& v, int j, long long dur,
+                                                     long long guard) {
+  for (++j; j < v.n; ++j) {
+    const long long st = v.lo[j];
+    if (st + dur <= usable_end(v, j, guard)) return st;
+    if (dur == 0 && j >= 1 && v.hi[j - 1] == st && usable_end(v, j - 1, guard) >= st) return st;
+  }
+  return kInf64;
+}
+
 struct ReqGeom {
   long long d0, d1, ovh;
   int extra;
@@ -289,15 +337,158 @@ __device__ bool ensure_private(const PackArgs& a, const TlSlot& sl, long long gb
   return true;
 }
 
-__global__ void __launch_bounds__(128) pack_kernel(PackArgs a) {
+// Upper bound on the usable room after time `a` on one GPU's gap list: the
+// largest usable_end - max(start, a) over gaps ending at or after a, or -1
+// when there is none (not even a zero-length interval fits).
+__device__ __forceinline__ long long room_after(const ListView& v, long long a, long long guard) {
+  long long best = -1;
+  for (int j = v.n - 1; j >= 0; --j) {
+    if (v.hi[j] < a) break;  // gaps are sorted: every earlier gap ends before a
+    const long long ue = usable_end(v, j, guard), lo = max(v.lo[j], a);
+    if (ue >= lo) best = max(best, ue - lo);
+  }
+  return best;
+}
+
+// Per-pipeline filter: every stage k of a request needs dur(k) <= room of its
+// GPU after the arrival. capA = min room over stages k < extra (duration d1),
+// capB = over k >= extra (d0). Rooms only shrink with commits (on the
+// pipeline's own GPUs) and with a later reference time, so a bound computed
+// at the minimum arrival of all requests still to come stays valid; it is
+// recomputed when the pipeline commits or fails a full search.
+__device__ __forceinline__ void pipeline_caps(const PackArgs& a, const TlSlot& sl, long long gb,
+                                              int pi, long long arrival, int extra,
+                                              long long& capA, long long& capB) {
+  const int S = sl.S, C = sl.C, D = sl.D;
+  const int pipe = pi / S, stage = pi % S;
+  const int li = (sl.Ce > 1 ? pipe : 0) * S + stage;
+  capA = kInf64;
+  capB = kInf64;
+  for (int k = 0; k < D; ++k) {
+    const ListView v = view_of(a, sl, gb, gpu_index(k, pipe, stage, C, S), li);
+    const long long r = room_after(v, arrival, a.guard_ns);
+    if (k < extra) capA = min(capA, r); else capB = min(capB, r);
+  }
+}
+
+// Group-parallel search: a group of gs lanes (power of two) evaluates one
+// pipeline; lane gl of the group owns stages k = gl, gl+gs, ... At the
+// current t every lane checks its stages' pieces [t+off_k, t+off_k+dur_k);
+// a piece that does not fit proposes the next start at which it could
+// (next_start - off_k); the group max of the proposals is the next t (no
+// feasible start lies below any proposal). The fixpoint is the earliest
+// common start t0 >= arrival, the minimum of the reference's candidate set
+// (bubbletea.cpp:164-188), or kInf64. Every lane of the warp must call it
+// (warp-synchronous); `pi < 0` marks an idle group.
+__device__ __forceinline__ long long group_search(const PackArgs& a, const TlSlot& sl,
+                                                  long long gb, int pi, long long arrival,
+                                                  const ReqGeom& rg, int gs, long long& iters) {
+  const int lane = threadIdx.x & 31, gl = lane & (gs - 1);
+  const int S = sl.S, C = sl.C, D = sl.D;
+  const int pipe = pi >= 0 ? pi / S : 0, stage = pi >= 0 ? pi % S : 0;
+  const int li = (sl.Ce > 1 ? pipe : 0) * S + stage;
+  long long t = pi >= 0 ? arrival : kInf64;
+  bool active = pi >= 0;
+  // the lane's first kP stages keep their list view and search cursor in
+  // registers for the whole search (t only grows; the lists do not change)
+  constexpr int kP = 4;
+  ListView vv[kP];
+  int cur[kP];
+#pragma unroll
+  for (int p = 0; p < kP; ++p) {
+    cur[p] = -2;
+    const int k = gl + p * gs;
+    if (active && k < D) vv[p] = view_of(a, sl, gb, gpu_index(k, pipe, stage, C, S), li);
+  }
+  while (__any_sync(kFull, active)) {
+    ++iters;
+    long long prop = t;
+    if (active) {
+#pragma unroll
+      for (int p = 0; p < kP; ++p) {
+        const int k = gl + p * gs;
+        if (k < D && prop != kInf64) {
+          const long long off = rg.off(k), dk = rg.dur(k);
+          const int j = last_start_le_from(vv[p], t + off, cur[p]);
+          if (!fits_at(vv[p], j, t + off, dk, a.guard_ns)) {
+            const long long st = next_start_from(vv[p], j, dk, a.guard_ns);
+            prop = st == kInf64 ? kInf64 : max(prop, st - off);
+          }
+        }
+      }
+      for (int k = gl + kP * gs; k < D && prop != kInf64; k += gs) {
+        const ListView v = view_of(a, sl, gb, gpu_index(k, pipe, stage, C, S), li);
+        const long long off = rg.off(k), dk = rg.dur(k);
+        if (fitting_gap(v, t + off, dk, a.guard_ns) < 0) {
+          const long long st = next_start(v, t + off, dk, a.guard_ns);
+          prop = st == kInf64 ? kInf64 : max(prop, st - off);
+        }
+      }
+    }
+    for (int o = gs >> 1; o > 0; o >>= 1) prop = max(prop, __shfl_xor_sync(kFull, prop, o));
+    if (active) {
+      if (prop == kInf64) {
+        t = kInf64;
+        active = false;
+      } else if (prop == t) {
+        active = false;  // every stage fits at t
+      } else {
+        t = prop;
+      }
+    }
+  }
+  return t;
+}
+
+// Caps of pipeline pi at reference time `a_ref`, group-parallel over its
+// stages (see pipeline_caps); every lane of the group gets the result.
+__device__ __forceinline__ void group_caps(const PackArgs& a, const TlSlot& sl, long long gb,
+                                           int pi, long long a_ref, int extra, int gs,
+                                           long long& capA, long long& capB) {
+  const int lane = threadIdx.x & 31, gl = lane & (gs - 1);
+  const int S = sl.S, C = sl.C, D = sl.D;
+  const int pipe = pi >= 0 ? pi / S : 0, stage = pi >= 0 ? pi % S : 0;
+  const int li = (sl.Ce > 1 ? pipe : 0) * S + stage;
+  capA = kInf64;
+  capB = kInf64;
+  if (pi >= 0) {
+    for (int k = gl; k < D; k += gs) {
+      const ListView v = view_of(a, sl, gb, gpu_index(k, pipe, stage, C, S), li);
+      const long long r = room_after(v, a_ref, a.guard_ns);
+      if (k < extra) capA = min(capA, r); else capB = min(capB, r);
+    }
+  }
+  for (int o = gs >> 1; o > 0; o >>= 1) {
+    capA = min(capA, __shfl_xor_sync(kFull, capA, o));
+    capB = min(capB, __shfl_xor_sync(kFull, capB, o));
+  }
+}
+
+// One warp per plan runs the FCFS request loop (schedule_prefills,
+// bubbletea.cpp:132-222). Requests are staged 32 at a time (one per lane:
+// load, durations, arrival check); a request is examined only if it passes
+// the warp-wide bound (some pipeline's caps admit its durations). The lanes
+// then filter 32 pipelines at a time by their caps and hand the survivors,
+// in pipeline order, to groups of lanes that search them concurrently;
+// first fit = the lowest feasible pipeline.
+__global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
+  extern __shared__ __align__(16) long long pk_smem[];
   const int lane = threadIdx.x & 31;
-  const int si = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int warp = threadIdx.x >> 5;
+  const int si = blockIdx.x * (blockDim.x >> 5) + warp;
   if (si >= a.n_slots) return;
   const TlSlot& sl = a.slots[si];
   const long long H = a.hz[si];
   const int D = sl.D, C = sl.C, S = sl.S, Ce = sl.Ce;
   const long long gb = a.gpu_base[si];
   const int G = D * C * S;
+  const int n_pipes = C * S;
+  int gs = 1;
+  while (gs < D && gs < 32) gs <<= 1;
+  const int ng = 32 / gs, grp = lane / gs, gl = lane & (gs - 1);
+  unsigned* memo = a.memo + (size_t)si * a.max_pipes * a.memo_words;
+  long long* capA = pk_smem + (size_t)warp * 2 * a.max_pipes;
+  long long* capB = capA + a.max_pipes;
   for (int i = lane; i < G; i += 32) a.gpu_off[gb + i] = -1;
   __syncwarp();
   const long long pool_base = (long long)si * a.pool_per_slot;
@@ -305,81 +496,163 @@ __global__ void __launch_bounds__(128) pack_kernel(PackArgs a) {
   // build_prefill_pipelines (bubbletea.cpp:88-130): layers per cell
   const int base_l = a.inf_layers / D, extra = a.inf_layers % D;
   const int total_layers = max(1, base_l * D + extra);
-  long long accepted = 0, rejected = 0;
+  long long accepted = 0;
   unsigned long long hash = 1469598103934665603ull;
-  const int n_pipes = C * S;
-  for (long long r = 0; r < a.n_req; ++r) {
-    const gpb_request q = a.reqs[r];
-    const long long arrival = ms_to_ns(q.arrival_ms);
-    int win = -1;
-    long long win_t = 0;
-    ReqGeom rg;
+  long long st_exam = 0, st_search = 0, st_fail = 0, st_iter = 0, st_cyc_search = 0,
+            st_cyc_caps = 0, st_cyc_commit = 0;
+  const long long st_t0 = clock64();
+  // initial caps, at the earliest arrival
+  const long long a0 = a.n_req > 0 ? a.sufmin[0] : 0;
+  for (int p0 = 0; p0 < n_pipes; p0 += ng) {
+    const int pi = p0 + grp < n_pipes ? p0 + grp : -1;
+    long long ca, cb;
+    group_caps(a, sl, gb, pi, a0, extra, gs, ca, cb);
+    if (pi >= 0 && gl == 0) {
+      capA[pi] = ca;
+      capB[pi] = cb;
+    }
+  }
+  __syncwarp();
+  long long mA = -kInf64, mB = -kInf64;
+  for (int pi = lane; pi < n_pipes; pi += 32) {
+    mA = max(mA, capA[pi]);
+    mB = max(mB, capB[pi]);
+  }
+  mA = warp_max64(mA);
+  mB = warp_max64(mB);
+  for (long long r0 = 0; r0 < a.n_req; r0 += 32) {
+    // stage 32 requests: durations (prefill_duration_ms :68-76, transfer
+    // :78-86, per-stage split :154-161)
+    const long long r = r0 + lane;
+    gpb_request q{};
+    long long arrival = kInf64;
+    ReqGeom rg{0, 0, 0, extra};
     double xfer = 0.0;
-    if (arrival <= H) {
-      // prefill_duration_ms (:68-76), transfer (:78-86), stage durations (:154-161)
-      const double dur_ms = __ddiv_rn(__dmul_rn(a.sat_ms, (double)q.tokens), (double)a.max_tokens);
-      const double bytes = (double)((long long)q.tokens * a.inf_hidden * a.bpe);
-      xfer = __dadd_rn(a.lat_ms, __ddiv_rn(bytes, a.stage_bw));
-      rg.ovh = ms_to_ns(xfer);
-      rg.d1 = ms_to_ns(__ddiv_rn(__dmul_rn(dur_ms, (double)(base_l + 1)), (double)total_layers));
-      rg.d0 = ms_to_ns(__ddiv_rn(__dmul_rn(dur_ms, (double)base_l), (double)total_layers));
-      rg.extra = extra;
-      for (int c0 = 0; c0 < n_pipes && win < 0; c0 += 32) {
-        const int pi = c0 + lane;
-        long long t_found = kInf64;
-        if (pi < n_pipes) {
-          const int pipe = pi / S, stage = pi % S;
-          const int li = (Ce > 1 ? pipe : 0) * S + stage;
-          long long t = arrival;
-          int ok_run = 0, k = 0;
-          while (ok_run < D) {
-            const ListView v = view_of(a, sl, gb, gpu_index(k, pipe, stage, C, S), li);
-            const long long off = rg.off(k), dk = rg.dur(k);
-            if (fitting_gap(v, t + off, dk, a.guard_ns) >= 0) {
-              ++ok_run;
-            } else {
-              const long long st = next_start(v, t + off, dk, a.guard_ns);
-              if (st == kInf64) {
-                t = kInf64;
-                break;
-              }
-              t = st - off;
-              ok_run = 1;
-            }
-            k = k + 1 == D ? 0 : k + 1;
-          }
-          t_found = t;
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, t_found != kInf64);
-        if (bal) {
-          const int src = __ffs(bal) - 1;
-          win = c0 + src;
-          win_t = __shfl_sync(0xffffffffu, t_found, src);
-        }
+    bool live = false;
+    if (r < a.n_req) {
+      q = a.reqs[r];
+      arrival = ms_to_ns(q.arrival_ms);
+      live = arrival <= H;  // later arrivals cannot fit before the horizon
+      if (live) {
+        const double dur_ms =
+            __ddiv_rn(__dmul_rn(a.sat_ms, (double)q.tokens), (double)a.max_tokens);
+        const double bytes = (double)((long long)q.tokens * a.inf_hidden * a.bpe);
+        xfer = __dadd_rn(a.lat_ms, __ddiv_rn(bytes, a.stage_bw));
+        rg.ovh = ms_to_ns(xfer);
+        rg.d1 = ms_to_ns(__ddiv_rn(__dmul_rn(dur_ms, (double)(base_l + 1)), (double)total_layers));
+        rg.d0 = ms_to_ns(__ddiv_rn(__dmul_rn(dur_ms, (double)base_l), (double)total_layers));
       }
     }
-    if (win >= 0) {
-      // commit (bubbletea.cpp:189-215): split the gap on each stage GPU
-      const int pipe = win / S, stage = win % S;
-      const int li = (Ce > 1 ? pipe : 0) * S + stage;
-      bool ovf = false;
-      // one lane commits (the per-warp bump allocator is serial); a
-      // zero-length interval at a gap end changes nothing (upper_bound
-      // insertion behind the span that ends the gap)
-      for (int k = 0; k < D && !ovf; ++k) {
-        const int gi = gpu_index(k, pipe, stage, C, S);
-        const long long lo = win_t + rg.off(k), hi = lo + rg.dur(k);
-        bool need = false;
-        if (lane == 0) {
-          const ListView v0 = view_of(a, sl, gb, gi, li);
-          const int j = fitting_gap(v0, lo, hi - lo, a.guard_ns);
-          need = j >= 0 && lo != v0.hi[j];
-          if (need && !ensure_private(a, sl, gb, gi, li, bump, pool_base)) ovf = true;
-          if (need && !ovf) {
+    const bool in_range = r < a.n_req;
+    unsigned todo = __ballot_sync(kFull, live && rg.d0 <= mB && (extra == 0 || rg.d1 <= mA));
+    unsigned won = 0;
+    long long my_start = -1;
+    int my_pipe = -1;
+    while (todo) {
+      ++st_exam;
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const long long arr = shfl_idx64(arrival, src);
+      const long long a_ref = a.sufmin[r0 + src];  // <= every arrival from here on
+      ReqGeom g2;
+      g2.d0 = shfl_idx64(rg.d0, src);
+      g2.d1 = shfl_idx64(rg.d1, src);
+      g2.ovh = shfl_idx64(rg.ovh, src);
+      g2.extra = extra;
+      const int tok = __shfl_sync(kFull, q.tokens, src) - 1;
+      int win = -1;
+      long long win_t = 0;
+      for (int c0 = 0; c0 < n_pipes && win < 0; c0 += 32) {
+        const int pl = c0 + lane;
+        bool cand = pl < n_pipes && g2.d0 <= capB[pl] && (extra == 0 || g2.d1 <= capA[pl]);
+        if (cand) cand = !((memo[(size_t)pl * a.memo_words + (tok >> 5)] >> (tok & 31)) & 1u);
+        unsigned pmask = __ballot_sync(kFull, cand);
+        while (pmask && win < 0) {
+          // the next ng survivors, in pipeline order, one per group
+          const unsigned bit = __fns(pmask, 0, grp + 1);
+          const int pi = bit < 32 ? c0 + (int)bit : -1;
+          st_search += pi >= 0 && gl == 0;
+          long long tc = clock64();
+          const long long t = group_search(a, sl, gb, pi, arr, g2, gs, st_iter);
+          st_cyc_search += clock64() - tc;
+          tc = clock64();
+          const unsigned ok = __ballot_sync(kFull, gl == 0 && pi >= 0 && t != kInf64);
+          if (ok) {
+            const int wl = __ffs(ok) - 1;  // lowest group = lowest pipeline
+            win = __shfl_sync(kFull, pi, wl);
+            win_t = shfl_idx64(t, wl);
+          }
+          // failed searches below the winner (or all): tighten their caps
+          const bool failed = pi >= 0 && t == kInf64 && (win < 0 || pi < win);
+          st_fail += failed && gl == 0;
+          // no start >= arr exists for this token count; every later request
+          // arrives at or after arr when arr is the minimum of the rest
+          if (failed && gl == 0 && arr == a_ref)
+            memo[(size_t)pi * a.memo_words + (tok >> 5)] |= 1u << (tok & 31);
+          if (__any_sync(kFull, failed)) {
+            long long ca, cb;
+            group_caps(a, sl, gb, failed ? pi : -1, a_ref, extra, gs, ca, cb);
+            if (failed && gl == 0) {
+              capA[pi] = ca;
+              capB[pi] = cb;
+            }
+          }
+          st_cyc_caps += clock64() - tc;
+          for (int g = 0; g < ng && pmask; ++g) pmask &= pmask - 1;
+        }
+      }
+      __syncwarp();
+      const long long tcm = clock64();
+      if (win >= 0) {
+        // commit (bubbletea.cpp:189-215): split the gap on each stage GPU,
+        // one lane per stage GPU; copy-on-write lists come from the slot's
+        // bump pool (warp prefix sum of the sizes)
+        const int pipe = win / S, stage = win % S;
+        const int li = (Ce > 1 ? pipe : 0) * S + stage;
+        bool ovf = false;
+        for (int k0 = 0; k0 < D && !ovf; k0 += 32) {
+          const int k = k0 + lane;
+          const int gi = k < D ? gpu_index(k, pipe, stage, C, S) : 0;
+          const long long lo = k < D ? win_t + g2.off(k) : 0, hi = k < D ? lo + g2.dur(k) : 0;
+          int j = -1, need = 0, ncap = 0, n = 0;
+          if (k < D) {
+            const ListView v0 = view_of(a, sl, gb, gi, li);
+            j = fitting_gap(v0, lo, hi - lo, a.guard_ns);
+            // a zero-length interval at a gap end changes nothing (upper_bound
+            // insertion behind the span that ends the gap)
+            need = j >= 0 && lo != v0.hi[j];
+            const long long off = a.gpu_off[gb + gi];
+            n = v0.n;
+            const int cap = off >= 0 ? a.gpu_cap[gb + gi] : 0;
+            if (need && !(off >= 0 && n + 1 <= cap)) ncap = max(2 * cap, n + 8);
+          }
+          int incl = ncap;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += v;
+          }
+          const int total = __shfl_sync(kFull, incl, 31);
+          if (bump + total > a.pool_per_slot) {
+            ovf = true;
+            break;
+          }
+          if (ncap > 0) {  // private copy with room
+            const long long noff = pool_base + bump + (incl - ncap);
+            const ListView v = view_of(a, sl, gb, gi, li);
+            for (int x = 0; x < n; ++x) {
+              a.pool_lo[noff + x] = v.lo[x];
+              a.pool_hi[noff + x] = v.hi[x];
+              a.pool_fl[noff + x] = v.fl[x];
+            }
+            a.gpu_off[gb + gi] = noff;
+            a.gpu_cnt[gb + gi] = n;
+            a.gpu_cap[gb + gi] = ncap;
+          }
+          bump += total;
+          if (need) {
             long long* L = a.pool_lo + a.gpu_off[gb + gi];
             long long* Hh = a.pool_hi + a.gpu_off[gb + gi];
             unsigned char* Fl = a.pool_fl + a.gpu_off[gb + gi];
-            int n = a.gpu_cnt[gb + gi];
             const long long glo = L[j], ghi = Hh[j];
             const unsigned char gfl = Fl[j];
             const int add_l = lo > glo, add_r = ghi > hi;
@@ -411,37 +684,70 @@ __global__ void __launch_bounds__(128) pack_kernel(PackArgs a) {
             }
             a.gpu_cnt[gb + gi] = n + delta;
           }
+          __syncwarp();
         }
-        ovf = __shfl_sync(0xffffffffu, (int)ovf, 0);
-      }
-      if (ovf) {
-        if (lane == 0) atomicExch(a.overflow, 1);
-        return;
-      }
-      ++accepted;
-      if (lane == 0) {
-        hash = fnv_mix(hash, (unsigned long long)(long long)q.id);
-        hash = fnv_mix(hash, (unsigned long long)(long long)win);
-        hash = fnv_mix(hash, (unsigned long long)win_t);
-        if (a.pl) {
-          gpb_placement& o = a.pl[(size_t)si * a.n_req + r];
-          o.start_ns = win_t;
-          o.ttft_overhead_ms = D - 1 == 0 ? 0.0 : __dmul_rn((double)(D - 1), xfer);
-          o.accepted = 1;
-          o.pipeline = win;
+        if (ovf) {
+          if (lane == 0) atomicExch(a.overflow, 1);
+          return;
+        }
+        ++accepted;
+        const int id = __shfl_sync(kFull, q.id, src);
+        if (lane == 0) {
+          hash = fnv_mix(hash, (unsigned long long)(long long)id);
+          hash = fnv_mix(hash, (unsigned long long)(long long)win);
+          hash = fnv_mix(hash, (unsigned long long)win_t);
+        }
+        if (lane == src) {
+          my_pipe = win;
+          my_start = win_t;
+        }
+        won |= 1u << src;
+        {  // the winner's GPU lists changed: its caps now
+          long long ca, cb;
+          group_caps(a, sl, gb, grp == 0 ? win : -1, a_ref, extra, gs, ca, cb);
+          if (lane == 0) {
+            capA[win] = ca;
+            capB[win] = cb;
+          }
         }
       }
-    } else {
-      ++rejected;
-      if (lane == 0 && a.pl) {
-        gpb_placement& o = a.pl[(size_t)si * a.n_req + r];
-        o.start_ns = -1;
-        o.ttft_overhead_ms = 0.0;
-        o.accepted = 0;
-        o.pipeline = -1;
+      __syncwarp();
+      st_cyc_commit += clock64() - tcm;
+      // caps only shrink: refresh the warp bounds and drop staged requests
+      // they no longer admit
+      long long ma = -kInf64, mb = -kInf64;
+      for (int pi = lane; pi < n_pipes; pi += 32) {
+        ma = max(ma, capA[pi]);
+        mb = max(mb, capB[pi]);
       }
+      mA = warp_max64(ma);
+      mB = warp_max64(mb);
+      todo &= __ballot_sync(kFull, live && rg.d0 <= mB && (extra == 0 || rg.d1 <= mA));
+    }
+    if (a.pl && in_range) {
+      gpb_placement& o = a.pl[(size_t)si * a.n_req + r];
+      const bool ok = (won >> lane) & 1u;
+      o.start_ns = ok ? my_start : -1;
+      o.ttft_overhead_ms = ok && D - 1 != 0 ? __dmul_rn((double)(D - 1), xfer) : 0.0;
+      o.accepted = ok ? 1 : 0;
+      o.pipeline = ok ? my_pipe : -1;
     }
     __syncwarp();
+  }
+  const long long rejected = a.n_req - accepted;
+  if (a.stats) {
+    st_search = (long long)__reduce_add_sync(kFull, (unsigned)st_search);
+    st_fail = (long long)__reduce_add_sync(kFull, (unsigned)st_fail);
+    if (lane == 0) {
+      a.stats[si * 8 + 0] = st_exam;
+      a.stats[si * 8 + 1] = st_search;
+      a.stats[si * 8 + 2] = st_fail;
+      a.stats[si * 8 + 3] = accepted;
+      a.stats[si * 8 + 4] = clock64() - st_t0;
+      a.stats[si * 8 + 5] = st_iter;
+      a.stats[si * 8 + 6] = st_cyc_search;
+      a.stats[si * 8 + 7] = st_cyc_caps * 1000000 / max(1LL, st_cyc_search) * 0 + st_cyc_commit;
+    }
   }
   // utilization before/after (bubbletea.cpp:224-238): per GPU busy = H - sum
   // of its gaps, summed in GPU-id order (DC in topology order, then cell,
@@ -819,13 +1125,26 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
   long long* dbase = (long long*)(gpu_cap + std::max(1LL, G));  // 16*G bytes in: aligned
   int* overflow = (int*)(dsum + std::max(1, n_rows_sel));
   cudaMemcpyAsync(dreq, reqs, sizeof(gpb_request) * n_req, cudaMemcpyHostToDevice, st);
+  c.sufmin_host.assign((size_t)n_req + 1, 0);
+  for (int64_t i = n_req - 1; i >= 0; --i) {
+    const long long t = host_ms_to_ns(reqs[i].arrival_ms);
+    c.sufmin_host[i] = i + 1 < n_req ? std::min(t, c.sufmin_host[i + 1]) : t;
+  }
+  long long* dsufmin = (long long*)c.dev_buf(c.b_sufmin, 8 * c.sufmin_host.size());
+  if (!dsufmin) return c.cuda_fail(cudaErrorMemoryAllocation, "pack buffers");
+  cudaMemcpyAsync(dsufmin, c.sufmin_host.data(), 8 * c.sufmin_host.size(), cudaMemcpyHostToDevice,
+                  st);
   cudaMemcpyAsync(dbase, gpu_base.data(), 8 * n_rows_sel, cudaMemcpyHostToDevice, st);
   gpb_placement* dpl = nullptr;
   if (placements) {
     dpl = (gpb_placement*)c.dev_buf(c.b_placements, sizeof(gpb_placement) * (size_t)n_rows_sel * std::max<int64_t>(1, n_req));
     if (!dpl) return c.cuda_fail(cudaErrorMemoryAllocation, "placements");
   }
-  long long pool = std::max(4096LL, 4 * max_nl);
+  // copy-on-write pool per slot: room for every GPU list to be copied twice
+  long long pool = 4096;
+  for (int i = 0; i < n_rows_sel; ++i)
+    pool = std::max(pool, 2 * (long long)slots[i].D * slots[i].C * slots[i].S *
+                              (2LL * slots[i].M + 1 + 16));
   for (int attempt = 0; attempt < 8; ++attempt) {
     long long* pool_lo = (long long*)c.dev_buf(c.b_tl_scratch, 17 * (size_t)pool * std::max(1, n_rows_sel));
     if (!pool_lo) return c.cuda_fail(cudaErrorMemoryAllocation, "pack pool");
@@ -844,6 +1163,7 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
     a.hz = c.tl_hz;
     a.reqs = dreq;
     a.n_req = n_req;
+    a.sufmin = dsufmin;
     a.sat_ms = pm->saturation_ms;
     a.stage_bw = pm->stage_bw;
     a.lat_ms = pm->boundary_latency_ms;
@@ -863,14 +1183,46 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
     a.sums = dsum;
     a.pl = dpl;
     a.overflow = overflow;
+    int max_pipes = 1;
+    for (const TlSlot& sl2 : slots) max_pipes = std::max(max_pipes, sl2.C * sl2.S);
+    a.max_pipes = max_pipes;
+    const size_t psmem = 4 * 2 * sizeof(long long) * (size_t)max_pipes;
+    if (psmem > (size_t)c.smem_optin) {
+      c.set_error("too many prefill pipelines per plan for the packing kernel");
+      return GPB_CONFIG_ERROR;
+    }
+    cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+    a.memo_words = (pm->max_tokens + 31) / 32;
+    const size_t memo_bytes = 4 * (size_t)a.memo_words * max_pipes * std::max(1, n_rows_sel);
+    a.memo = (unsigned*)c.dev_buf(c.b_pack_memo, memo_bytes);
+    if (!a.memo) return c.cuda_fail(cudaErrorMemoryAllocation, "pack memo");
+    cudaMemsetAsync(a.memo, 0, memo_bytes, st);
+    a.stats = nullptr;
+    if (std::getenv("GPB_PACK_STATS")) {
+      a.stats = (long long*)c.dev_buf(c.b_pack_stats, 64 * (size_t)std::max(1, n_rows_sel));
+      cudaMemsetAsync(a.stats, 0, 64 * (size_t)std::max(1, n_rows_sel), st);
+    }
     cudaMemsetAsync(overflow, 0, 4, st);
-    pack_kernel<<<(n_rows_sel + 3) / 4, 128, 0, st>>>(a);
+    pack_kernel<<<(n_rows_sel + 3) / 4, 128, psmem, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return c.cuda_fail(e, "pack launch");
     int32_t ovf = 0;
     cudaMemcpyAsync(&ovf, overflow, 4, cudaMemcpyDeviceToHost, st);
     cudaEventRecord(c.ev3, st);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return c.cuda_fail(e, "pack");
+    if (a.stats) {
+      std::vector<long long> hs(8 * (size_t)n_rows_sel);
+      cudaMemcpy(hs.data(), a.stats, 64 * (size_t)n_rows_sel, cudaMemcpyDeviceToHost);
+      long long tot[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mx = 0;
+      for (int i = 0; i < n_rows_sel; ++i) {
+        for (int k = 0; k < 8; ++k) tot[k] += hs[8 * i + k];
+        mx = std::max(mx, hs[8 * i + 4]);
+      }
+      std::fprintf(stderr, "pack stats (attempt %d, pool %lld, ovf %d): examined %lld searches %lld "
+                   "failed %lld accepted %lld cycles sum %lld max %lld; search iters %lld "
+                   "search cyc %lld commit cyc %lld\n", attempt, pool, ovf,
+                   tot[0], tot[1], tot[2], tot[3], tot[4], mx, tot[5], tot[6], tot[7]);
+    }
     if (!ovf) break;
     if (attempt == 7) {
       c.set_error("gap pool overflow");

@@ -65,13 +65,14 @@ struct Ctx {
   bool profile_rows = false;
   // timeline / bubbletea buffers
   Buf b_tl_rows, b_tl_spans, b_tl_nspan, b_tl_scratch, b_gaps, b_ngaps, b_reqs, b_pl,
-      b_sum, b_pack_scratch, b_pack_misc;
+      b_sum, b_pack_scratch, b_pack_misc, b_sufmin, b_pack_stats, b_pack_memo;
 
   std::vector<cudaEvent_t> bucket_ev;      // [buckets + 1] bucket start (+ fork)
   std::vector<cudaEvent_t> bucket_ev_end;  // [buckets]
   std::vector<cudaStream_t> side;          // concurrent bucket streams
   std::vector<cudaEvent_t> side_done;
   Buf b_placements, b_ar;
+  std::vector<long long> sufmin_host;  // pack: suffix-min arrivals (pinned by the call)
   bool pack_allreduce = false;  // include the all-reduce tail in timelines
   // last build_timelines() outputs (device pointers into the buffers above)
   long long *tl_glo = nullptr, *tl_ghi = nullptr, *tl_gsum = nullptr, *tl_hz = nullptr;
@@ -85,7 +86,7 @@ struct Ctx {
   std::vector<Buf*> all_bufs() {
     return {&b_topos, &b_scens, &b_row_scen, &b_work, &b_rows, &b_results, &b_cursors,
             &b_best, &b_scratch, &b_cycles, &b_tl_rows, &b_tl_spans, &b_tl_nspan, &b_tl_scratch,
-            &b_gaps, &b_ngaps, &b_reqs, &b_pl, &b_sum, &b_pack_scratch, &b_pack_misc,
+            &b_gaps, &b_ngaps, &b_reqs, &b_pl, &b_sum, &b_pack_scratch, &b_pack_misc, &b_sufmin, &b_pack_stats, &b_pack_memo,
             &b_placements, &b_ar};
   }
 

@@ -126,3 +126,41 @@ def test_synthetic_requests_match_reference(checker):
     a = list(synthetic_requests(1000, 42, 1234.5, pm))
     b = ref.synthetic(1000, 42, 1234.5, pm)
     assert [(x.id, x.tokens, x.arrival_ms) for x in a] == [(x.id, x.tokens, x.arrival_ms) for x in b]
+
+
+def test_pack_config2_top_plans_long_trace(planner, checker):
+    """BubbleTea at a config-4-like shape: the best plans of the bench's
+    config-2 space, one shared synthetic trace whose arrivals span the largest
+    makespan, most requests rejected; summaries and placements bit-exact."""
+    from paper_2411_14458_b200 import workloads
+    topos, scens = workloads.config2(2_000, seed=3)
+    tarr = abi.array(abi.Topology, topos)
+    planner.load(tarr, abi.array(abi.Scenario, scens))
+    planner.evaluate()
+    rows = planner.rows()
+    # the best plans with at most 8 cells (the reference's packing cost grows
+    # with D^2 per request; the GPU path is D-parallel)
+    feas = sorted(((r.throughput, i) for i, r in enumerate(rows[:planner.n_rows])
+                   if r.feasible == 1 and r.d <= 8), key=lambda x: (-x[0], x[1]))
+    pols = {}
+    top = []
+    for _, i in feas:  # a few plans of every policy
+        pol = scens[rows[i].scenario].policy
+        if pols.get(pol, 0) < 2:
+            pols[pol] = pols.get(pol, 0) + 1
+            top.append(i)
+    pm = abi.PrefillModel.default()
+    hmax = max(rows[i].makespan_ns for i in top) / 1e6
+    reqs = list(synthetic_requests(4_000, 7, hmax, pm))
+    got, gpl = planner.pack_prefills(top, reqs, pm, placements=True)
+    n = len(reqs)
+    for k, i in enumerate(top):
+        sc = scens[rows[i].scenario]
+        want, wpl = checker.pack(tarr, sc, rows[i].d, reqs, pm)
+        g = got[k]
+        assert (g.accepted, g.rejected, g.placement_hash, g.utilization_before,
+                g.utilization_after) == (want.accepted, want.rejected, want.placement_hash,
+                                         want.utilization_before, want.utilization_after), k
+        for a, b in zip(gpl[k * n:(k + 1) * n], wpl):
+            assert (a.accepted, a.pipeline, a.start_ns, a.ttft_overhead_ms) == \
+                (b.accepted, b.pipeline, b.start_ns, b.ttft_overhead_ms)
