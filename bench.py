@@ -140,7 +140,7 @@ def impl_reference(args):
     }
     if not args.no_bubbletea:
         line["bubbletea"] = bt_reference()
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -502,14 +502,34 @@ def impl_ours(args):
                 line["bubbletea"]["cpu_baseline"] = {"value": v, "unit": "pairs/s",
                                                      "cores": cores, "kind": kind,
                                                      "sample": sample}
-        print(json.dumps(line), flush=True)
+        emit(line)
     planner.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
+def _stdout_for_json_only():
+    """The driver reads exactly one JSON line from stdout: libraries (NCCL's
+    version banner, warnings) write to fd 1 too, so fd 1 is pointed at
+    stderr and the JSON goes through a private duplicate of the original."""
+    global _JSON_OUT
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
+
+
+_JSON_OUT = None
+
+
+def emit(line):
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    _stdout_for_json_only()
     args = parse()
     if args.impl == "reference":
         return impl_reference(args)
