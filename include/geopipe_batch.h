@@ -278,6 +278,7 @@ typedef struct gpb_bucket_info {
   int32_t policy, B, rows, max_s, max_c, max_m, stream, pad_;
   float start_ms;              /* launch-stream fork -> bucket start */
   float ms;                    /* bucket kernel duration */
+  double algo_ops;             /* algorithmic max-plus ops of its feasible rows */
 } gpb_bucket_info;
 int gpb_bucket_infos(gpb_ctx* ctx, gpb_bucket_info* out, int32_t cap, int32_t* n);
 

@@ -95,7 +95,7 @@ class BucketInfo(C.Structure):
     _fields_ = [("policy", C.c_int32), ("B", C.c_int32), ("rows", C.c_int32),
                 ("max_s", C.c_int32), ("max_c", C.c_int32), ("max_m", C.c_int32),
                 ("stream", C.c_int32), ("pad_", C.c_int32), ("start_ms", C.c_float),
-                ("ms", C.c_float)]
+                ("ms", C.c_float), ("algo_ops", C.c_double)]
 
 
 class Best(C.Structure):

@@ -997,6 +997,16 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
 
 }  // namespace
 
+namespace gpb {
+// WAN boundaries of a row's plan (DC blocks - 1), or -1 if infeasible.
+int row_wan_boundaries(const Ctx& c, int64_t row) {
+  const int si = c.row_scen_host[row];
+  const DevScen& sc = c.dev_scens_host[si];
+  const HostBlocks hb = host_decode(sc, c.dev_topos_host[sc.topo], (int)(row - sc.first_row) + 1);
+  return hb.feasible ? hb.nb - 1 : -1;
+}
+}  // namespace gpb
+
 extern "C" int gpb_bubbles(gpb_ctx* ctx_, int64_t row, int64_t horizon_ns, gpb_bubble* out,
                            int64_t cap, int64_t* n_out) {
   if (!ctx_) return GPB_ERROR;

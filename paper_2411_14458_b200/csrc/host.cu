@@ -415,6 +415,7 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   c.dev_scens_host = ds;
   c.dev_topos_host = dt;
   c.row_scen_host = row_scen;
+  c.work_host = work;
   if (cudaStreamSynchronize(st) != cudaSuccess) return c.cuda_fail(cudaGetLastError(), "upload");
   c.loaded = true;
   if (n_rows_out) *n_rows_out = n_rows;
@@ -643,6 +644,18 @@ int gpb_bucket_infos(gpb_ctx* ctx_, gpb_bucket_info* out, int32_t cap, int32_t* 
     o.max_c = b.max_c;
     o.max_m = b.max_m;
     o.stream = b.stream;
+    // algorithmic max-plus ops of the bucket's feasible rows
+    double ops = 0;
+    for (int32_t k = 0; k < b.count; ++k) {
+      const int64_t row = c.work_host[b.offset + k];
+      const int W = row_wan_boundaries(c, row);
+      if (W < 0) continue;
+      const DevScen& d = c.dev_scens_host[c.row_scen_host[row]];
+      const double SM = (double)d.S * d.M, WM = (double)W * d.M;
+      ops += d.policy == GPB_ATLAS ? d.C * (4 * SM + 6 * WM)
+                                   : (d.policy == GPB_1F1B ? 4 * SM : 5 * SM) + 6 * WM;
+    }
+    o.algo_ops = ops;
     if (c.timing_valid) {
       cudaEventElapsedTime(&o.start_ms, c.bucket_ev[c.buckets.size()], c.bucket_ev[bi]);
       cudaEventElapsedTime(&o.ms, c.bucket_ev[bi], c.bucket_ev_end[bi]);

@@ -58,6 +58,7 @@ struct Ctx {
   std::vector<DevScen> dev_scens_host;
   std::vector<DevTopo> dev_topos_host;
   std::vector<int32_t> row_scen_host;
+  std::vector<int32_t> work_host;  // bucket work lists (profiling)
 
   // device tables
   Buf b_topos, b_scens, b_row_scen, b_work, b_rows, b_results, b_cursors, b_best;
@@ -106,5 +107,7 @@ struct AtlasPlan {
 };
 int plan_atlas(Ctx& c, int B, bool timeline, int C, int S, int M, int nw, long long max_csm,
                long long count, AtlasPlan& P);
+
+int row_wan_boundaries(const Ctx& c, int64_t row);
 
 }  // namespace gpb
