@@ -14,9 +14,11 @@ struct AtlasLayout {
   long long garr_cap;  // gradient-queue entries kept in shared memory per warp
                        // (rows with C*S*M above it use the global scratch)
   // outputs
-  size_t off_wa, off_wg, off_wbs, off_gf, off_cand, off_lastc, off_nm, off_done,
-      off_firstm, off_pub_nm, off_pub_last, off_pub_done, off_fdl, off_resf, off_resb,
-      off_hint, off_mf, off_mb, off_mtmp, off_mcnt, off_garr, total;
+  bool big_in_smem = true;  // lists in the shared slice (else the global scratch)
+  size_t off_wa, off_wg, off_wbs, off_gf, off_nm, off_firstm, off_mcnt, off_big, off_garr,
+      total;
+  // "big" region (lists), relative to its base
+  size_t off_fdl, off_resf, off_resb, off_mf, off_mb, off_mtmp, big_total;
   int cap;             // list storage per WAN boundary = C * M (C lists of M)
 
   __host__ __device__ static size_t al(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -25,27 +27,24 @@ struct AtlasLayout {
     const size_t CS = (size_t)C * S;
     cap = C * M;
     size_t o = 0;
-    off_wa = o;        o = al(o + 16 * 8);          // a_w [0,8) | ser_w [8,16)
-    off_wg = o;        o = al(o + 16 * 8);          // G_w [0,8) | lat_w [8,16)
-    off_wbs = o;       o = al(o + (size_t)S * 4);   // WAN boundary before stage s
-    off_gf = o;        o = al(o + CS * 8);
-    off_cand = o;      o = al(o + CS * 8);
-    off_lastc = o;     o = al(o + (size_t)S * 8);
-    off_nm = o;        o = al(o + CS * 4);
-    off_done = o;      o = al(o + (size_t)S * 4);
-    off_firstm = o;    o = al(o + CS * 4);
-    off_pub_nm = o;    o = al(o + (size_t)C * 32 * 4);
-    off_pub_last = o;  o = al(o + 32 * 8);
-    off_pub_done = o;  o = al(o + 32 * 4);
-    off_fdl = o;       o = al(o + (size_t)C * M * 8);
-    off_resf = o;      o = al(o + (size_t)nw * cap * 8);
+    off_fdl = o;       o = al(o + (size_t)C * M * 8);   // last-stage forward ends
+    off_resf = o;      o = al(o + (size_t)nw * cap * 8);  // per-pipeline link lists
     off_resb = o;      o = al(o + (size_t)nw * cap * 8);
-    off_hint = o;      o = al(o + (size_t)2 * (nw > 0 ? nw : 1) * C * 4);  // search cursors
     // merged static lists (pipelines < p) per WAN link, forward / gradient
     off_mf = o;        o = al(o + (size_t)nw * cap * 8);
     off_mb = o;        o = al(o + (size_t)nw * cap * 8);
     off_mtmp = o;      o = al(o + (size_t)cap * 8);
-    off_mcnt = o;      o = al(o + 32 * 4);                // counts / cursors
+    big_total = o;
+    o = 0;
+    off_wa = o;        o = al(o + 16 * 8);          // a_w [0,8) | ser_w [8,16)
+    off_wg = o;        o = al(o + 16 * 8);          // G_w [0,8) | lat_w [8,16)
+    off_wbs = o;       o = al(o + (size_t)S * 4);   // WAN boundary before stage s
+    off_gf = o;        o = al(o + CS * 8);
+    off_nm = o;        o = al(o + CS * 4);
+    off_firstm = o;    o = al(o + CS * 4);
+    off_mcnt = o;      o = al(o + 32 * 4);          // counts / cursors
+    off_big = o;
+    if (big_in_smem) o = al(o + big_total);
     off_garr = o;
     o = al(o + (size_t)garr_cap * 8);
     total = o;

@@ -955,6 +955,7 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
       const int grid = P.grid, wpc = P.wpc;
       a.scratch = nullptr;
       a.scratch_per_warp = P.scratch_per_warp;
+      a.scratch_big_off = P.scratch_big_off;
       if (P.scratch_per_warp > 0) {
         a.scratch = (long long*)c.dev_buf(c.b_tl_scratch,
                                           8 * (size_t)P.scratch_per_warp * grid * wpc);

@@ -514,7 +514,7 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     a.cursor = cursors + bi;
     a.rows = (gpb_row*)c.b_rows.ptr;
     a.error_flag = err_flag;
-    a.row_cycles = c.profile_rows ? (long long*)c.dev_buf(c.b_cycles, 72 * (size_t)c.n_rows)
+    a.row_cycles = c.profile_rows ? (long long*)c.dev_buf(c.b_cycles, 136 * (size_t)c.n_rows)
                                   : nullptr;
     a.row_phase = a.row_cycles ? a.row_cycles + c.n_rows : nullptr;
     const int grid = std::min(grid_eval, (b.count + 3) / 4);
@@ -533,6 +533,7 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
       const AtlasPlan& P = aplan[bi];
       a.lay = P.L;
       a.scratch_per_warp = P.scratch_per_warp;
+      a.scratch_big_off = P.scratch_big_off;
       a.scratch = P.scratch_per_warp > 0 ? (long long*)c.b_scratch.ptr + scr_off[bi] : nullptr;
       const int agrid = P.grid, wpc = P.wpc;
       e = launch_atlas(b.B, a, agrid, wpc, st);
@@ -749,9 +750,9 @@ extern "C" int gpb_fetch_row_cycles(gpb_ctx* ctx_, int64_t* out, int64_t n) {
     return GPB_CONFIG_ERROR;
   }
   cudaSetDevice(c.device);
-  // out: n row costs followed by n x 4 atlas phase costs (when n == 5 * rows)
+  // out: n row costs followed by n x 16 atlas phase counters (when n == 17 * rows)
   const int64_t rows = c.n_rows;
-  n = std::min(n, 9 * rows);
+  n = std::min(n, 17 * rows);
   cudaError_t e = cudaMemcpyAsync(out, c.b_cycles.ptr, 8 * (size_t)n, cudaMemcpyDeviceToHost,
                                   c.stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
@@ -785,6 +786,12 @@ int plan_atlas(Ctx& c, int B, bool timeline, int C, int S, int M, int nw, long l
     L.compute();
   }
   P.wpc = (int)std::min<size_t>(4, (size_t)c.smem_optin / L.total);
+  if (P.wpc < 1) {  // lists too large for the slice: they go to the global scratch
+    L.big_in_smem = false;
+    L.garr_cap = 0;
+    L.compute();
+    P.wpc = (int)std::min<size_t>(4, (size_t)c.smem_optin / L.total);
+  }
   if (P.wpc < 1) {
     c.set_error("atlas plan too large for the shared-memory slice");
     return GPB_CONFIG_ERROR;
@@ -794,7 +801,8 @@ int plan_atlas(Ctx& c, int B, bool timeline, int C, int S, int M, int nw, long l
   per_sm = std::max(1, std::min(per_sm, (int)(sm_budget / smem)));
   P.grid = (int)std::max(1LL, std::min<long long>((long long)c.num_sms * per_sm,
                                                   (count + P.wpc - 1) / P.wpc));
-  P.scratch_per_warp = L.garr_cap < max_csm ? max_csm : 0;
+  P.scratch_big_off = L.garr_cap < max_csm ? max_csm : 0;
+  P.scratch_per_warp = P.scratch_big_off + (L.big_in_smem ? 0 : (long long)(L.big_total / 8));
   return GPB_OK;
 }
 

@@ -103,7 +103,8 @@ struct Ctx {
 struct AtlasPlan {
   AtlasLayout L;
   int wpc = 0, grid = 0;
-  long long scratch_per_warp = 0;  // global gradient-queue entries per warp
+  long long scratch_per_warp = 0;  // int64 per warp of global scratch: queues + lists
+  long long scratch_big_off = 0;   // int64 offset of the lists (when not in shared memory)
 };
 int plan_atlas(Ctx& c, int B, bool timeline, int C, int S, int M, int nw, long long max_csm,
                long long count, AtlasPlan& P);

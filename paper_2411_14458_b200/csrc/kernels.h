@@ -37,7 +37,8 @@ struct EvalArgs {
   // atlas: per-warp shared slice and (when it does not fit) global garr
   AtlasLayout lay;
   long long* scratch;
-  long long scratch_per_warp; // int64 elements per warp (global garr)
+  long long scratch_per_warp; // int64 elements per warp (global garr + lists)
+  long long scratch_big_off;  // int64 offset of the lists inside a warp's scratch
 };
 
 struct SelectArgs {

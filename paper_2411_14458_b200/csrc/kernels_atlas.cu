@@ -34,46 +34,7 @@
 
 namespace gpb {
 
-constexpr int kAtlasQ = 2;  // commits per stage per wavefront round
-
 // ------------------------------------------------------- union of lists
-
-// first index i of a sorted start array with st[i] + len > x. Queries on one
-// link arrive in nearly increasing time order, so the search starts at the
-// per-(link, pipeline) cursor `h` (when given) and walks a few entries
-// either way before falling back to bisection; the cursor is updated.
-__device__ __forceinline__ int first_end_after(const long long* st, int n, long long len,
-                                               long long x, int* h = nullptr) {
-  int lo = 0, hi = n;
-  int i = h ? max(0, min(*h, n)) : n;
-  if (i > 0 && st[i - 1] + len > x) {  // answer < i: walk back
-    hi = i - 1;
-#pragma unroll 1
-    for (int k = 0; k < 6; ++k) {
-      if (hi == 0 || st[hi - 1] + len <= x) {
-        lo = hi;
-        break;
-      }
-      --hi;
-    }
-  } else {  // answer >= i: walk forward
-    lo = i;
-#pragma unroll 1
-    for (int k = 0; k < 6; ++k) {
-      if (lo == n || st[lo] + len > x) {
-        hi = lo;
-        break;
-      }
-      ++lo;
-    }
-  }
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (st[mid] + len > x) hi = mid; else lo = mid + 1;
-  }
-  if (h) *h = lo;
-  return lo;
-}
 
 // Counts of the C per-pipeline arrays of one link.
 struct LinkCounts {
@@ -82,53 +43,11 @@ struct LinkCounts {
   int p, m;        // pipeline whose count is overridden by m (-1: none)
   int mode;        // 0: res_bwd counts from nm; 1: res_fwd (q<p: M, q==p: m)
   int M;
-  int* hint;       // per-pipeline search cursors of this link, or nullptr
-  __device__ __forceinline__ int* cur(int q) const { return hint ? hint + q : nullptr; }
   __device__ __forceinline__ int count(int q) const {
     if (mode == 1) return q < p ? M : (q == p ? m : 0);
     return q == p ? m : nm[q * S + s];
   }
 };
-
-// earliest_fit (base.h:75-84) over the union.
-__device__ __forceinline__ long long union_earliest_fit(const long long* base, int C, int M,
-                                                        const LinkCounts& k, long long lo,
-                                                        long long len) {
-  if (len <= 0) return lo;
-  long long t = lo;
-  for (;;) {
-    bool changed = false;
-    for (int q = 0; q < C; ++q) {
-      const int n = k.count(q);
-      if (n == 0) continue;
-      const long long* st = base + (size_t)q * M;
-      if (st[n - 1] + len <= t) continue;
-      int i = first_end_after(st, n, len, t, k.cur(q));
-      while (i < n && st[i] < t + len) {
-        t = st[i] + len;
-        ++i;
-        changed = true;
-      }
-    }
-    if (!changed) return t;
-  }
-}
-
-// free_at (base.h:65-72) over the union.
-__device__ __forceinline__ bool union_free_at(const long long* base, int C, int M,
-                                              const LinkCounts& k, long long start,
-                                              long long len) {
-  if (len <= 0) return true;
-  for (int q = 0; q < C; ++q) {
-    const int n = k.count(q);
-    if (n == 0) continue;
-    const long long* st = base + (size_t)q * M;
-    if (st[n - 1] + len <= start) continue;
-    const int i = first_end_after(st, n, len, start, k.cur(q));
-    if (i < n && st[i] < start + len) return false;
-  }
-  return true;
-}
 
 // latest_fit (base.h:88-99) over the union, ignoring entry (skip_q, skip_i)
 // (the pair's own reservation, unreserved by the caller).
@@ -162,86 +81,36 @@ __device__ __forceinline__ long long union_latest_fit(const long long* base, int
   }
 }
 
-// free_at over the union, one lane per pipeline list (warp-uniform result).
-__device__ __forceinline__ bool warp_union_free_at(const long long* base, int C, int M,
-                                                   const LinkCounts& k, long long start,
-                                                   long long len) {
-  if (len <= 0) return true;
-  bool conflict = false;
-  for (int q = threadIdx.x & 31; q < C; q += 32) {
-    const int n = k.count(q);
-    if (n == 0) continue;
-    const long long* st = base + (size_t)q * M;
-    if (st[n - 1] + len <= start) continue;
-    const int i = first_end_after(st, n, len, start, k.cur(q));
-    if (i < n && st[i] < start + len) conflict = true;
-  }
-  return !__any_sync(0xffffffffu, conflict);
-}
-
-// earliest_fit over the union: every lane pushes t past the overlapping run
-// of its own list; the warp max of the proposals keeps "no feasible start in
-// [lo, t)" invariant, and the fixpoint is the reference's answer.
-__device__ __forceinline__ long long warp_union_earliest_fit(const long long* base, int C, int M,
-                                                             const LinkCounts& k, long long lo,
-                                                             long long len) {
-  if (len <= 0) return lo;
-  long long t = lo;
-  for (;;) {
-    long long my = t;
-    for (int q = threadIdx.x & 31; q < C; q += 32) {
-      const int n = k.count(q);
-      if (n == 0) continue;
-      const long long* st = base + (size_t)q * M;
-      if (st[n - 1] + len <= my) continue;
-      int i = first_end_after(st, n, len, my, k.cur(q));
-      while (i < n && st[i] < my + len) {
-        my = st[i] + len;
-        ++i;
-      }
-    }
-    long long nt = my;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nt = imax(nt, __shfl_xor_sync(0xffffffffu, nt, o));
-    if (nt == t) return t;
-    t = nt;
-  }
-}
-
 // ------------------------------------------------------------ the warp
 
 struct AtlasMem {
-  long long *wa, *wg, *gf, *cand, *lastc, *fdl, *resf, *resb, *garr, *pub_last;
+  long long *wa, *wg, *gf, *fdl, *resf, *resb, *garr;
   long long *garr_smem, *garr_glob;
   long long garr_cap;
-  int *wbs, *nm, *done, *firstm, *pub_nm, *pub_done, *hintf, *hintb;
+  int *wbs, *nm, *firstm;
   long long *mf, *mb, *mtmp;  // merged static link lists (forward phase)
   int* mcnt;                  // [w] |mf|, [8+w] |mb|, [16+w] mb cursor
   long long* fe;  // timeline: forward ends [C][S][M] (global)
   long long* ps;  // timeline: pair starts  [C][S][M] (global)
 
-  __device__ void carve(unsigned char* base, const AtlasLayout& L, long long* garr_global) {
+  // small state in the warp's shared slice; the lists ("big" region) there
+  // too when they fit, else in the warp's global scratch
+  __device__ void carve(unsigned char* base, const AtlasLayout& L, long long* garr_global,
+                        unsigned char* big_global) {
     wa = (long long*)(base + L.off_wa);
     wg = (long long*)(base + L.off_wg);
     wbs = (int*)(base + L.off_wbs);
     gf = (long long*)(base + L.off_gf);
-    cand = (long long*)(base + L.off_cand);
-    lastc = (long long*)(base + L.off_lastc);
     nm = (int*)(base + L.off_nm);
-    done = (int*)(base + L.off_done);
     firstm = (int*)(base + L.off_firstm);
-    pub_nm = (int*)(base + L.off_pub_nm);
-    pub_last = (long long*)(base + L.off_pub_last);
-    pub_done = (int*)(base + L.off_pub_done);
-    fdl = (long long*)(base + L.off_fdl);
-    resf = (long long*)(base + L.off_resf);
-    resb = (long long*)(base + L.off_resb);
-    hintf = (int*)(base + L.off_hint);
-    hintb = hintf + (L.nw > 0 ? L.nw : 1) * L.C;
-    mf = (long long*)(base + L.off_mf);
-    mb = (long long*)(base + L.off_mb);
-    mtmp = (long long*)(base + L.off_mtmp);
     mcnt = (int*)(base + L.off_mcnt);
+    unsigned char* big = L.big_in_smem ? base + L.off_big : big_global;
+    fdl = (long long*)(big + L.off_fdl);
+    resf = (long long*)(big + L.off_resf);
+    resb = (long long*)(big + L.off_resb);
+    mf = (long long*)(big + L.off_mf);
+    mb = (long long*)(big + L.off_mb);
+    mtmp = (long long*)(big + L.off_mtmp);
     garr_smem = (long long*)(base + L.off_garr);
     garr_glob = garr_global;
     garr_cap = L.garr_cap;
@@ -249,18 +118,6 @@ struct AtlasMem {
     fe = ps = nullptr;
   }
 };
-
-// Candidate start of pair (p, s, m): atlas_pair_start(max(ready, gpu_free))
-// (scheduler.cpp:461-485, 287-294); the caller guarantees readiness.
-__device__ __forceinline__ long long atlas_cand(const Geom& g, const AtlasMem& X, int p, int s,
-                                                int m, int wb, long long serb) {
-  const int S = g.S, M = g.M, C = g.C;
-  const long long ready = s == S - 1 ? X.fdl[p * M + m] : X.garr[((size_t)p * S + s) * M + m];
-  const long long lo = imax(ready, X.gf[p * S + s]);
-  if (wb < 0) return lo;
-  LinkCounts k{X.nm, S, s, -1, 0, 0, M, X.hintb + wb * C};
-  return union_earliest_fit(X.resb + (size_t)wb * C * M, C, M, k, lo + g.dur, serb) - g.dur;
-}
 
 // ------------------------------------------- forward-phase link lists
 //
@@ -297,11 +154,29 @@ __device__ __forceinline__ void warp_merge(long long* A, int na, const long long
   __syncwarp();
 }
 
+// Advance the cursor to the first static entry ending after x (gallop from
+// the cursor, then bisect).
+__device__ __forceinline__ void link_advance(const long long* mg, int n, int& cur, long long len,
+                                             long long x) {
+  if (cur >= n || mg[cur] + len > x) return;
+  int lo = cur + 1, step = 1;
+  while (lo + step - 1 < n && mg[lo + step - 1] + len <= x) {
+    lo += step;
+    step <<= 1;
+  }
+  int hi = min(lo + step - 1, n);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (mg[mid] + len <= x) lo = mid + 1; else hi = mid;
+  }
+  cur = lo;
+}
+
 // [x, x+len) overlaps a static entry (cursor `cur`, advanced) or the own tail
 __device__ __forceinline__ bool link_conflict(const long long* mg, int n, int& cur,
                                               long long own_last, long long len, long long x) {
   if (len <= 0) return false;
-  while (cur < n && mg[cur] + len <= x) ++cur;
+  link_advance(mg, n, cur, len, x);
   if (cur < n && mg[cur] < x + len) return true;
   return own_last + len > x;
 }
@@ -312,7 +187,7 @@ __device__ __forceinline__ long long link_fit(const long long* mg, int n, int& c
   if (len <= 0) return x;
   long long t = x;
   for (;;) {
-    while (cur < n && mg[cur] + len <= t) ++cur;
+    link_advance(mg, n, cur, len, t);
     if (cur < n && mg[cur] < t + len) {
       t = mg[cur] + len;
       continue;
@@ -362,9 +237,12 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
                                               long long (&gfr)[B], int (&drr)[B],
                                               const int (&wbi)[B], const long long (&serb)[B],
                                               const long long (&latb)[B], long long& n_pairs,
-                                              long long& n_scans, long long& n_rounds) {
+                                              long long& n_scans, long long& n_rounds,
+                                              long long* cph) {
+  long long ct = cph ? clock64() : 0;
   const int lane = threadIdx.x & 31;
   const int S = g.S, M = g.M, C = g.C;
+  const int nl = (S + B - 1) / B;  // lanes owning stages
   const long long dur = g.dur;
   // lowest blocked stage
   int my_min = 0x7fffffff;
@@ -397,6 +275,11 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
   for (int j = 0; j < B; ++j) wl[j] = wbi[j] >= 0 ? serb[j] + latb[j] : 0;
 
   n_rounds += R;
+  if (cph) {
+    const long long t1 = clock64();
+    cph[0] += t1 - ct;
+    ct = t1;
+  }
   for (int r = 0; r < R; ++r) {
     long long xin[B], dl[B];
 #pragma unroll
@@ -410,6 +293,11 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
       }
     }
     long long lo[B];
+    if (cph) {
+      const long long t1 = clock64();
+      cph[1] += t1 - ct;
+      ct = t1;
+    }
     for (;;) {
       ++n_scans;
       // lane map: stages lane*B+B-1 (applied first) down to lane*B
@@ -430,17 +318,17 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
         ta = mp_add(ta, fa);
         tb = imax(mp_add(tb, fa), fb);
       }
-      // inclusive suffix scan over lanes (higher lanes = deeper stages first)
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
+      // inclusive suffix scan over the nl stage-owning lanes (higher lanes =
+      // deeper stages first)
+      for (int o = 1; o < nl; o <<= 1) {
         const long long oa = shfl_down64(ta, o), ob = shfl_down64(tb, o);
-        if (lane + o < 32) {
+        if (lane + o < nl) {
           tb = imax(mp_add(ob, ta), tb);
           ta = mp_add(oa, ta);
         }
       }
       long long v = shfl_down64(tb, 1);  // everything above this lane, at -inf
-      if (lane == 31) v = kNegMP;
+      if (lane + 1 >= nl) v = kNegMP;
       // evaluate the lane's stages; check the WAN links at their inputs
       int conf = -1;
       long long conf_y = 0;
@@ -478,6 +366,11 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
           if (j == conf) dl[j] += fit - conf_y;
       }
     }
+    if (cph) {
+      const long long t1 = clock64();
+      cph[2] += t1 - ct;
+      ct = t1;
+    }
     // commit the round
 #pragma unroll
     for (int j = 0; j < B; ++j) {
@@ -492,6 +385,11 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
       if (TIMELINE) X.ps[((size_t)p * S + s) * M + k] = t;
     }
     __syncwarp();
+    if (cph) {
+      const long long t1 = clock64();
+      cph[3] += t1 - ct;
+      ct = t1;
+    }
   }
 #pragma unroll
   for (int j = 0; j < B; ++j) drr[j] += cnt[j];
@@ -659,6 +557,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
   const int lane = threadIdx.x & 31;
   long long ph_casc = 0, ph_chain = 0, ph_fit = 0, ph_drain = 0, ph_t = 0;
   long long n_stage_it = 0, n_pairs = 0, n_adm = 0, n_rounds = 0;
+  long long cph[4] = {0, 0, 0, 0};  // cascade: setup, loads, scan rounds, commits
   const int S = g.S, M = g.M, C = g.C;
   const long long f = g.fwd, dur = g.dur;
   const int nw = g.nb - 1;
@@ -667,11 +566,9 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     X.gf[i] = 0;
     X.nm[i] = 0;
   }
-  for (int i = lane; i < nw * C; i += 32) X.hintf[i] = X.hintb[i] = 0;
   for (int s = lane; s < S; s += 32) {
     int w;
     X.wbs[s] = (s > 0 && wan_after(g, s - 1, w)) ? w : -1;
-    X.done[s] = 0;
   }
   if (lane < nw) {  // pooled serialization / latency per WAN boundary
     X.wa[8 + lane] = g.ser_pooled[lane];
@@ -680,13 +577,14 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
   __syncwarp();
 
   // Per-lane stage info and chain offsets a_s (lane prefix + warp scan).
-  int wbi[B];
+  const int nl = (S + B - 1) / B;  // lanes owning stages
+  int wbi[B], wfi[B];  // WAN boundary before / after the stage, or -1
   long long serb[B], latb[B], a_loc[B];
   long long run = 0;
 #pragma unroll
   for (int j = 0; j < B; ++j) {
     const int s = lane * B + j;
-    wbi[j] = -1;
+    wbi[j] = wfi[j] = -1;
     serb[j] = latb[j] = 0;
     a_loc[j] = run;
     if (s < S) {
@@ -697,7 +595,10 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
         latb[j] = g.lat[w];
       }
       run += f;
-      if (s + 1 < S && wan_after(g, s, w)) run += g.ser_pooled[w] + g.lat[w];
+      if (s + 1 < S && wan_after(g, s, w)) {
+        run += g.ser_pooled[w] + g.lat[w];
+        wfi[j] = w;
+      }
     }
   }
   {
@@ -755,7 +656,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
       nblk = __reduce_add_sync(kFull, nblk);
       if (nblk > 0) {
         atlas_cascade<B, TIMELINE>(g, p, m, mem_limit, X, gfr, drr, wbi, serb, latb, n_pairs,
-                                   n_stage_it, n_rounds);
+                                   n_stage_it, n_rounds, phase ? cph : nullptr);
         ++n_adm;
       }
       if (phase) {
@@ -772,8 +673,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
         gl[j] = runmax;
       }
       long long pre = runmax;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
+      for (int o = 1; o < nl; o <<= 1) {
         const long long v = shfl_up64(pre, o);
         if (lane >= o) pre = imax(pre, v);
       }
@@ -782,11 +682,9 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
 #pragma unroll
       for (int j = 0; j < B; ++j) {
         gl[j] = imax(gl[j], prev);
-        const int s = lane * B + j;
-        int w;
-        if (s + 1 < S && wan_after(g, s, w)) {
-          X.wa[w] = a_loc[j];
-          X.wg[w] = gl[j];
+        if (wfi[j] >= 0) {
+          X.wa[wfi[j]] = a_loc[j];
+          X.wg[wfi[j]] = gl[j];
         }
       }
       long long t0 = __shfl_sync(kFull, gfr[0], 0);  // gpu_free of stage 0
@@ -883,6 +781,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     phase[5] = n_pairs;
     phase[6] = n_adm;
     phase[7] = n_rounds;
+    for (int k = 0; k < 4; ++k) phase[8 + k] = cph[k];
   }
   // -------------------------------------------- right-pack (timeline)
   if (TIMELINE) {
@@ -928,8 +827,9 @@ __global__ void __launch_bounds__(kEvalThreads, 1) atlas_kernel(EvalArgs a) {
   const int warp = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
   AtlasMem X;
-  X.carve(smem + (size_t)warp * a.lay.total, a.lay,
-          a.scratch ? a.scratch + (size_t)gwarp * a.scratch_per_warp : nullptr);
+  long long* scr = a.scratch ? a.scratch + (size_t)gwarp * a.scratch_per_warp : nullptr;
+  X.carve(smem + (size_t)warp * a.lay.total, a.lay, scr,
+          scr ? (unsigned char*)(scr + a.scratch_big_off) : nullptr);
   for (;;) {
     const int wk = next_work(a.cursor);
     if (wk >= a.n_work) break;
@@ -941,7 +841,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) atlas_kernel(EvalArgs a) {
     if (!begin_row(a, row, g, sc, tp)) continue;
     int err = 0;
     const long long mk = atlas_row<B, false>(g, sc->mem_limit, X, err,
-                                             a.row_phase ? a.row_phase + 8 * (size_t)row : nullptr);
+                                             a.row_phase ? a.row_phase + 16 * (size_t)row : nullptr);
     end_row(a, row, g, *sc, *tp, mk, err, t_start);
     __syncwarp();
   }
@@ -953,8 +853,9 @@ __global__ void __launch_bounds__(kEvalThreads, 1) atlas_timeline_kernel(EvalArg
   const int warp = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
   AtlasMem X;
-  X.carve(smem + (size_t)warp * a.lay.total, a.lay,
-          a.scratch ? a.scratch + (size_t)gwarp * a.scratch_per_warp : nullptr);
+  long long* scr = a.scratch ? a.scratch + (size_t)gwarp * a.scratch_per_warp : nullptr;
+  X.carve(smem + (size_t)warp * a.lay.total, a.lay, scr,
+          scr ? (unsigned char*)(scr + a.scratch_big_off) : nullptr);
   for (;;) {
     const int wk = next_work(a.cursor);
     if (wk >= a.n_work) break;

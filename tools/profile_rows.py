@@ -17,12 +17,12 @@ p.evaluate()
 p.evaluate()
 rows = p.rows()
 import ctypes as C
-raw = (C.c_int64 * (9 * n))()
-p._check(p.lib.gpb_fetch_row_cycles(p.ctx, raw, 9 * n))
+raw = (C.c_int64 * (17 * n))()
+p._check(p.lib.gpb_fetch_row_cycles(p.ctx, raw, 17 * n))
 cyc = list(raw[:n])
-phase = [list(raw[n + 8 * i: n + 8 * i + 8]) for i in range(n)]
+phase = [list(raw[n + 16 * i: n + 16 * i + 16]) for i in range(n)]
 t = p.timing()
-agg = collections.defaultdict(lambda: [0, 0, 0, [0] * 8])
+agg = collections.defaultdict(lambda: [0, 0, 0, [0] * 16])
 for r, c, ph in zip(rows[:n], cyc, phase):
     s = scens[r.scenario]
     S = (s.num_layers + s.layers_per_partition - 1) // s.layers_per_partition
@@ -32,12 +32,13 @@ for r, c, ph in zip(rows[:n], cyc, phase):
     a[1] += c
     a[2] = max(a[2], c)
     if s.policy == 3:
-        for k in range(8):
+        for k in range(16):
             a[3][k] += ph[k]
 tot = sum(v[1] for v in agg.values())
 print(json.dumps({"evaluate_ms": t.evaluate_ms, "policy_ms": list(t.policy_ms)}))
 print("policy S C M feas | rows  sum_Mcyc  share  max_kcyc")
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:25]:
-    ph = [round(x / max(1, v[1]) * 100) for x in v[3][:4]] + [round(x / v[0]) for x in v[3][4:8]]
+    ph = [round(x / max(1, v[1]) * 100) for x in v[3][:4]] + [round(x / v[0]) for x in v[3][4:8]] \
+        + [round(x / max(1, v[1]) * 100) for x in v[3][8:12]]
     print(*k, "|", v[0], round(v[1] / 1e6, 2), f"{100 * v[1] / tot:.1f}%", round(v[2] / 1e3, 1),
-          "phases% casc/chain/fit/drain + per-row scans/pairs/adm/rounds", ph)
+          "phases% casc/chain/fit/drain + per-row scans/pairs/adm/rounds + casc% setup/loads/scan/commit", ph)
