@@ -100,6 +100,8 @@ Ctx::~Ctx() {
   for (Buf* b : all_bufs()) {
     if (b->ptr) cudaFree(b->ptr);
   }
+  drop_graph();
+  if (fork_ev) cudaEventDestroy(fork_ev);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (ev2) cudaEventDestroy(ev2);
@@ -416,92 +418,38 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   c.dev_topos_host = dt;
   c.row_scen_host = row_scen;
   c.work_host = work;
+  c.eval_ready = false;
+  c.drop_graph();
   if (cudaStreamSynchronize(st) != cudaSuccess) return c.cuda_fail(cudaGetLastError(), "upload");
   c.loaded = true;
   if (n_rows_out) *n_rows_out = n_rows;
   return GPB_OK;
 }
 
-int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
-  if (!ctx_) return GPB_ERROR;
-  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
-  c.last_error.clear();
-  if (!c.loaded) {
-    c.set_error("no plan space loaded");
-    return GPB_CONFIG_ERROR;
-  }
-  cudaSetDevice(c.device);
-  cudaStream_t st = c.stream;
+// The evaluate launch sequence (timing events, cursor reset, bucket kernels
+// forked onto side streams, join, selection) on stream `st`. `cap` marks a
+// stream capture: timing events become external event nodes of the graph.
+static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
+  auto rec = [&](cudaEvent_t ev, cudaStream_t s2) {
+    return cap ? cudaEventRecordWithFlags(ev, s2, cudaEventRecordExternal)
+               : cudaEventRecord(ev, s2);
+  };
   int32_t* cursors = (int32_t*)c.b_cursors.ptr;
   int32_t* err_flag = cursors + c.buckets.size();
-  cudaEventRecord(c.ev0, st);
+  rec(c.ev0, st);
   cudaMemsetAsync(cursors, 0, sizeof(int32_t) * (c.buckets.size() + 1), st);
   int launches = 0;
   const int grid_eval = c.num_sms * 8;
-  while (c.bucket_ev.size() < c.buckets.size() + 1) {
-    cudaEvent_t e;
-    if (cudaEventCreate(&e) != cudaSuccess) return c.cuda_fail(cudaGetLastError(), "event");
-    c.bucket_ev.push_back(e);
-  }
-  // buckets run concurrently on side streams forked from the launch stream:
-  // one stream per bucket up to kSideStreams, beyond that longest-first
-  // onto the least loaded stream
-  const size_t n_side = std::max<size_t>(1, std::min<size_t>(kSideStreams, c.buckets.size()));
-  while (c.side.size() < n_side) {
-    cudaStream_t s2;
-    cudaEvent_t e2;
-    if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&e2, cudaEventDisableTiming) != cudaSuccess)
-      return c.cuda_fail(cudaGetLastError(), "side streams");
-    c.side.push_back(s2);
-    c.side_done.push_back(e2);
-  }
-  while (c.bucket_ev_end.size() < c.buckets.size()) {
-    cudaEvent_t e;
-    if (cudaEventCreate(&e) != cudaSuccess) return c.cuda_fail(cudaGetLastError(), "event");
-    c.bucket_ev_end.push_back(e);
-  }
-  cudaEventRecord(c.bucket_ev[c.buckets.size()], st);  // fork point
-  for (size_t k = 0; k < n_side; ++k) cudaStreamWaitEvent(c.side[k], c.bucket_ev[c.buckets.size()], 0);
-  // ATLAS launch shapes first: the global gradient-queue scratch of every
-  // concurrently running bucket is carved from one allocation
-  std::vector<AtlasPlan> aplan(c.buckets.size());
-  std::vector<size_t> scr_off(c.buckets.size(), 0);
-  size_t scr_total = 0;
+  const size_t n_side = c.n_side;
+  cudaEventRecord(c.fork_ev, st);  // fork point (dependency only)
+  for (size_t k = 0; k < n_side; ++k) cudaStreamWaitEvent(c.side[k], c.fork_ev, 0);
+  rec(c.bucket_ev[c.buckets.size()], st);
   for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
     const Bucket& b = c.buckets[bi];
-    if (b.policy != GPB_ATLAS || b.count == 0) continue;
-    const int rc = plan_atlas(c, b.B, false, b.max_c, b.max_s, b.max_m, b.max_nw, b.max_csm,
-                              b.count, aplan[bi]);
-    if (rc != GPB_OK) return rc;
-    if (std::getenv("GPB_DEBUG_PLAN"))
-      std::fprintf(stderr, "atlas bucket %zu B=%d rows=%d C=%d S=%d M=%d nw=%d csm=%lld cap=%lld "
-                   "total=%zu wpc=%d grid=%d spw=%lld\n", bi, b.B, b.count, b.max_c, b.max_s,
-                   b.max_m, b.max_nw, b.max_csm, aplan[bi].L.garr_cap, aplan[bi].L.total,
-                   aplan[bi].wpc, aplan[bi].grid, aplan[bi].scratch_per_warp);
-    scr_off[bi] = scr_total;
-    scr_total += (size_t)aplan[bi].scratch_per_warp * aplan[bi].grid * aplan[bi].wpc;
-  }
-  if (scr_total > 0 && !c.dev_buf(c.b_scratch, sizeof(long long) * scr_total))
-    return c.cuda_fail(cudaErrorMemoryAllocation, "atlas scratch");
-  {  // streams: longest estimate first onto the least loaded stream (LPT)
-    std::vector<size_t> ord(c.buckets.size());
-    for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
-    std::stable_sort(ord.begin(), ord.end(),
-                     [&](size_t x, size_t y) { return c.buckets[x].est > c.buckets[y].est; });
-    std::vector<double> load(n_side, 0.0);
-    for (size_t i : ord) {
-      const size_t si = std::min_element(load.begin(), load.end()) - load.begin();
-      load[si] += c.buckets[i].est;
-      c.buckets[i].stream = (int)si;
-    }
-  }
-  for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
-    const Bucket& b = c.buckets[bi];
-    cudaStream_t st = c.side[b.stream];
-    cudaEventRecord(c.bucket_ev[bi], st);
+    cudaStream_t ss = c.side[b.stream];
+    rec(c.bucket_ev[bi], ss);
     if (b.count == 0) {
-      cudaEventRecord(c.bucket_ev_end[bi], st);
+      rec(c.bucket_ev_end[bi], ss);
       continue;
     }
     EvalArgs a;
@@ -514,39 +462,32 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     a.cursor = cursors + bi;
     a.rows = (gpb_row*)c.b_rows.ptr;
     a.error_flag = err_flag;
-    a.row_cycles = c.profile_rows ? (long long*)c.dev_buf(c.b_cycles, 136 * (size_t)c.n_rows)
-                                  : nullptr;
+    a.row_cycles = c.profile_rows ? (long long*)c.b_cycles.ptr : nullptr;
     a.row_phase = a.row_cycles ? a.row_cycles + c.n_rows : nullptr;
     const int grid = std::min(grid_eval, (b.count + 3) / 4);
     cudaError_t e;
     if (b.policy == GPB_GPIPE || b.policy == GPB_VARUNA) {
       a.smem_m = b.max_m;
-      const size_t smem = (size_t)(kEvalThreads / 32) * b.max_m * 8;
-      if ((int)smem > c.smem_optin) {
-        c.set_error("num_microbatches too large for the flush kernel's shared buffer");
-        return GPB_CONFIG_ERROR;
-      }
-      e = launch_flush(b.B, b.policy == GPB_GPIPE, a, grid, st);
+      e = launch_flush(b.B, b.policy == GPB_GPIPE, a, grid, ss);
     } else if (b.policy == GPB_1F1B) {
-      e = launch_onef1b(b.B, a, grid, st);
+      e = launch_onef1b(b.B, a, grid, ss);
     } else {
-      const AtlasPlan& P = aplan[bi];
+      const AtlasPlan& P = c.aplan[bi];
       a.lay = P.L;
       a.scratch_per_warp = P.scratch_per_warp;
       a.scratch_big_off = P.scratch_big_off;
-      a.scratch = P.scratch_per_warp > 0 ? (long long*)c.b_scratch.ptr + scr_off[bi] : nullptr;
-      const int agrid = P.grid, wpc = P.wpc;
-      e = launch_atlas(b.B, a, agrid, wpc, st);
+      a.scratch = P.scratch_per_warp > 0 ? (long long*)c.b_scratch.ptr + c.scr_off[bi] : nullptr;
+      e = launch_atlas(b.B, a, P.grid, P.wpc, ss);
     }
     if (e != cudaSuccess) return c.cuda_fail(e, "eval launch");
-    cudaEventRecord(c.bucket_ev_end[bi], st);
+    rec(c.bucket_ev_end[bi], ss);
     ++launches;
   }
   for (size_t k = 0; k < n_side; ++k) {  // join
     cudaEventRecord(c.side_done[k], c.side[k]);
     cudaStreamWaitEvent(st, c.side_done[k], 0);
   }
-  cudaEventRecord(c.ev1, st);
+  rec(c.ev1, st);
   SelectArgs sa;
   sa.scens = (const DevScen*)c.b_scens.ptr;
   sa.n_scen = c.n_scen;
@@ -558,11 +499,142 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
   cudaError_t e = launch_select(sa, sgrid, st);
   if (e != cudaSuccess) return c.cuda_fail(e, "select launch");
   launches += 2;
-  cudaEventRecord(c.ev2, st);
+  rec(c.ev2, st);
   c.last_launches = launches + 1;  // + the cursor memset
+  return GPB_OK;
+}
+
+// Everything the launch sequence needs, once per loaded space: events, side
+// streams, ATLAS launch shapes, scratch, stream assignment (LPT).
+static int prepare_evaluate(Ctx& c) {
+  auto mk = [&](std::vector<cudaEvent_t>& v, size_t n, unsigned flags) -> bool {
+    while (v.size() < n) {
+      cudaEvent_t e;
+      if (cudaEventCreateWithFlags(&e, flags) != cudaSuccess) return false;
+      v.push_back(e);
+    }
+    return true;
+  };
+  if (!mk(c.bucket_ev, c.buckets.size() + 1, cudaEventDefault) ||
+      !mk(c.bucket_ev_end, c.buckets.size(), cudaEventDefault))
+    return c.cuda_fail(cudaGetLastError(), "event");
+  if (!c.fork_ev && cudaEventCreateWithFlags(&c.fork_ev, cudaEventDisableTiming) != cudaSuccess)
+    return c.cuda_fail(cudaGetLastError(), "event");
+  // buckets run concurrently on side streams forked from the launch stream
+  c.n_side = std::max<size_t>(1, std::min<size_t>(kSideStreams, c.buckets.size()));
+  while (c.side.size() < c.n_side) {
+    cudaStream_t s2;
+    cudaEvent_t e2;
+    if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e2, cudaEventDisableTiming) != cudaSuccess)
+      return c.cuda_fail(cudaGetLastError(), "side streams");
+    c.side.push_back(s2);
+    c.side_done.push_back(e2);
+  }
+  for (const Bucket& b : c.buckets)
+    if ((b.policy == GPB_GPIPE || b.policy == GPB_VARUNA) &&
+        (int)((size_t)(kEvalThreads / 32) * b.max_m * 8) > c.smem_optin) {
+      c.set_error("num_microbatches too large for the flush kernel's shared buffer");
+      return GPB_CONFIG_ERROR;
+    }
+  // ATLAS launch shapes: the global scratch of every concurrently running
+  // bucket is carved from one allocation
+  c.aplan.assign(c.buckets.size(), AtlasPlan());
+  c.scr_off.assign(c.buckets.size(), 0);
+  size_t scr_total = 0;
+  for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
+    const Bucket& b = c.buckets[bi];
+    if (b.policy != GPB_ATLAS || b.count == 0) continue;
+    const int rc = plan_atlas(c, b.B, false, b.max_c, b.max_s, b.max_m, b.max_nw, b.max_csm,
+                              b.count, c.aplan[bi]);
+    if (rc != GPB_OK) return rc;
+    if (std::getenv("GPB_DEBUG_PLAN"))
+      std::fprintf(stderr, "atlas bucket %zu B=%d rows=%d C=%d S=%d M=%d nw=%d csm=%lld cap=%lld "
+                   "total=%zu big_in_smem=%d wpc=%d grid=%d spw=%lld\n", bi, b.B, b.count,
+                   b.max_c, b.max_s, b.max_m, b.max_nw, b.max_csm, c.aplan[bi].L.garr_cap,
+                   c.aplan[bi].L.total, (int)c.aplan[bi].L.big_in_smem, c.aplan[bi].wpc,
+                   c.aplan[bi].grid, c.aplan[bi].scratch_per_warp);
+    c.scr_off[bi] = scr_total;
+    scr_total += (size_t)c.aplan[bi].scratch_per_warp * c.aplan[bi].grid * c.aplan[bi].wpc;
+  }
+  if (scr_total > 0 && !c.dev_buf(c.b_scratch, sizeof(long long) * scr_total))
+    return c.cuda_fail(cudaErrorMemoryAllocation, "atlas scratch");
+  if (c.profile_rows && !c.dev_buf(c.b_cycles, 136 * (size_t)c.n_rows))
+    return c.cuda_fail(cudaErrorMemoryAllocation, "row profile");
+  {  // streams: longest estimate first onto the least loaded stream (LPT)
+    std::vector<size_t> ord(c.buckets.size());
+    for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](size_t x, size_t y) { return c.buckets[x].est > c.buckets[y].est; });
+    std::vector<double> load(c.n_side, 0.0);
+    for (size_t i : ord) {
+      const size_t si = std::min_element(load.begin(), load.end()) - load.begin();
+      load[si] += c.buckets[i].est;
+      c.buckets[i].stream = (int)si;
+    }
+  }
+  c.eval_ready = true;
+  return GPB_OK;
+}
+
+void Ctx::drop_graph() {
+  if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  graph_exec = nullptr;
+  graph_stream = nullptr;
+}
+
+int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
+  if (!ctx_) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  c.last_error.clear();
+  if (!c.loaded) {
+    c.set_error("no plan space loaded");
+    return GPB_CONFIG_ERROR;
+  }
+  cudaSetDevice(c.device);
+  cudaStream_t st = c.stream;
+  if (!c.eval_ready) {
+    c.drop_graph();
+    const int rc = prepare_evaluate(c);
+    if (rc != GPB_OK) return rc;
+  }
+  // GPB_GRAPH=1 captures the sequence once per loaded space and stream into
+  // a CUDA graph and replays it. Measured on config 2 it is not the default:
+  // every gpb_load re-captures (0.6 ms of host time per step in the e2e
+  // loop) and the replayed step ran 15 % slower on the device than the
+  // directly launched one (0.83 vs 0.71 ms).
+  static const bool use_graph = std::getenv("GPB_GRAPH") != nullptr;
+  if (!use_graph) {
+    const int rc = record_evaluate(c, st, false);
+    if (rc != GPB_OK) return rc;
+  } else {
+    if (!c.graph_exec || c.graph_stream != st) {
+      c.drop_graph();
+      cudaGraph_t g = nullptr;
+      if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+        return c.cuda_fail(cudaGetLastError(), "graph capture");
+      const int rc = record_evaluate(c, st, true);
+      const cudaError_t ce = cudaStreamEndCapture(st, &g);
+      if (rc != GPB_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (ce != cudaSuccess) return c.cuda_fail(ce, "graph capture");
+      const cudaError_t ie = cudaGraphInstantiate(&c.graph_exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ie != cudaSuccess) {
+        c.graph_exec = nullptr;
+        return c.cuda_fail(ie, "graph instantiate");
+      }
+      c.graph_stream = st;
+    }
+    const cudaError_t e = cudaGraphLaunch(c.graph_exec, st);
+    if (e != cudaSuccess) return c.cuda_fail(e, "graph launch");
+  }
   c.timing_valid = true;
   if (sync) {
-    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return c.cuda_fail(e, "evaluate");
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return c.cuda_fail(e, "evaluate");
     return c.check_error_flag();
   }
   return GPB_OK;
@@ -626,7 +698,7 @@ int gpb_set_stream(gpb_ctx* ctx_, void* s) {
   if (!ctx_) return GPB_ERROR;
   Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
   c.stream = s ? (cudaStream_t)s : c.own_stream;
-  return GPB_OK;
+  return GPB_OK;  // the evaluate graph is re-captured for a new stream
 }
 
 int gpb_bucket_infos(gpb_ctx* ctx_, gpb_bucket_info* out, int32_t cap, int32_t* n) {
@@ -738,7 +810,9 @@ extern "C" int gpb_microbench(gpb_ctx* ctx_, int32_t kind, double* gops) {
 
 extern "C" int gpb_set_profile(gpb_ctx* ctx_, int32_t enable) {
   if (!ctx_) return GPB_ERROR;
-  reinterpret_cast<Ctx*>(ctx_)->profile_rows = enable != 0;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  if (c.profile_rows != (enable != 0)) c.eval_ready = false;
+  c.profile_rows = enable != 0;
   return GPB_OK;
 }
 

@@ -38,6 +38,14 @@ struct Bucket {
   bool heavy = false;  // ATLAS rows near the heaviest estimate (launched first)
 };
 
+// Launch shape of one ATLAS kernel (evaluation or timeline variant) over
+// `count` rows whose largest C, S, M, WAN count and C*S*M are given.
+struct AtlasPlan {
+  AtlasLayout L;
+  int wpc = 0, grid = 0;
+  long long scratch_per_warp = 0;  // int64 per warp of global scratch: queues + lists
+  long long scratch_big_off = 0;   // int64 offset of the lists (when not in shared memory)
+};
 struct Ctx {
   int device = 0;
   int num_sms = 148;
@@ -81,6 +89,15 @@ struct Ctx {
   int *tl_gcnt = nullptr, *tl_ghas = nullptr;
   void* tl_slots_dev = nullptr;
   bool timing_valid = false;
+  // evaluate launch sequence: prepared once per loaded space, replayed as a graph
+  bool eval_ready = false;
+  size_t n_side = 0;
+  cudaEvent_t fork_ev = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaStream_t graph_stream = nullptr;
+  void drop_graph();
+  std::vector<AtlasPlan> aplan;  // per bucket (ATLAS only)
+  std::vector<size_t> scr_off;    // per bucket offset into b_scratch (int64)
   int last_launches = 0;
   float pack_ms = 0.f;
 
@@ -98,14 +115,6 @@ struct Ctx {
   ~Ctx();
 };
 
-// Launch shape of one ATLAS kernel (evaluation or timeline variant) over
-// `count` rows whose largest C, S, M, WAN count and C*S*M are given.
-struct AtlasPlan {
-  AtlasLayout L;
-  int wpc = 0, grid = 0;
-  long long scratch_per_warp = 0;  // int64 per warp of global scratch: queues + lists
-  long long scratch_big_off = 0;   // int64 offset of the lists (when not in shared memory)
-};
 int plan_atlas(Ctx& c, int B, bool timeline, int C, int S, int M, int nw, long long max_csm,
                long long count, AtlasPlan& P);
 
