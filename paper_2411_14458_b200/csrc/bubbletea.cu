@@ -1151,11 +1151,15 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
     dpl = (gpb_placement*)c.dev_buf(c.b_placements, sizeof(gpb_placement) * (size_t)n_rows_sel * std::max<int64_t>(1, n_req));
     if (!dpl) return c.cuda_fail(cudaErrorMemoryAllocation, "placements");
   }
-  // copy-on-write pool per slot: room for every GPU list to be copied twice
+  // copy-on-write pool per slot. Final list sizes are bounded by the initial
+  // gaps plus one split per accepted request on each of its D stage GPUs;
+  // capacity doubling at most triples the total. An overflow re-runs the
+  // kernel with 4x the pool, so the first size errs on the large side.
   long long pool = 4096;
-  for (int i = 0; i < n_rows_sel; ++i)
-    pool = std::max(pool, 2 * (long long)slots[i].D * slots[i].C * slots[i].S *
-                              (2LL * slots[i].M + 1 + 16));
+  for (int i = 0; i < n_rows_sel; ++i) {
+    const long long G = (long long)slots[i].D * slots[i].C * slots[i].S;
+    pool = std::max(pool, 3 * (G * (2LL * slots[i].M + 9) + (long long)slots[i].D * n_req));
+  }
   for (int attempt = 0; attempt < 8; ++attempt) {
     long long* pool_lo = (long long*)c.dev_buf(c.b_tl_scratch, 17 * (size_t)pool * std::max(1, n_rows_sel));
     if (!pool_lo) return c.cuda_fail(cudaErrorMemoryAllocation, "pack pool");
@@ -1228,6 +1232,18 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
       for (int i = 0; i < n_rows_sel; ++i) {
         for (int k = 0; k < 8; ++k) tot[k] += hs[8 * i + k];
         mx = std::max(mx, hs[8 * i + 4]);
+      }
+      std::vector<int> ord(n_rows_sel);
+      for (int i = 0; i < n_rows_sel; ++i) ord[i] = i;
+      std::sort(ord.begin(), ord.end(), [&](int x, int y) { return hs[8 * x + 4] > hs[8 * y + 4]; });
+      for (int q = 0; q < std::min(n_rows_sel, 4); ++q) {
+        const int i = ord[q];
+        const TlSlot& sl = slots[i];
+        std::fprintf(stderr, "  slot %d row %lld pol %d D %d C %d S %d M %d: cycles %lld examined %lld "
+                     "searches %lld failed %lld accepted %lld iters %lld search_cyc %lld\n", i,
+                     (long long)sl.row, sl.policy, sl.D, sl.C, sl.S, sl.M, hs[8 * i + 4],
+                     hs[8 * i], hs[8 * i + 1], hs[8 * i + 2], hs[8 * i + 3], hs[8 * i + 5],
+                     hs[8 * i + 6]);
       }
       std::fprintf(stderr, "pack stats (attempt %d, pool %lld, ovf %d): examined %lld searches %lld "
                    "failed %lld accepted %lld cycles sum %lld max %lld; search iters %lld "
