@@ -299,6 +299,42 @@ __device__ __forceinline__ long long next_start_from(const ListView& v, int j, l
   return kInf64;
 }
 
+// The shared (never copied) gap list li of a slot.
+__device__ __forceinline__ ListView base_view(const PackArgs& a, const TlSlot& sl, int li) {
+  ListView v;
+  const long long go = sl.gap_off + (long long)li * (2 * sl.M + 1);
+  v.lo = a.glo + go;
+  v.hi = a.ghi + go;
+  v.fl = a.gflag + go;
+  v.n = a.gcnt[sl.lst_off + li];
+  return v;
+}
+
+// Zero-length pieces at x_i = x0 + i*step (i < cnt) against one gap list: the
+// shift to add to t so that the first failing piece reaches its next allowed
+// point (next_start, bubbletea.cpp:164-188 for dur 0), 0 if every piece
+// fits, kInf64 if one never can. A zero-length piece at x fits iff x lies in
+// some gap's closed usable interval [lo, usable_end] (incl. the touching rule).
+__device__ __forceinline__ long long zero_run_shift(const ListView& v, long long x0,
+                                                    long long step, int cnt, long long guard) {
+  int j = last_start_le(v, x0);
+  long long i = 0;
+  for (;;) {
+    const long long x = x0 + i * step;
+    while (j + 1 < v.n && v.lo[j + 1] <= x) ++j;
+    if (!fits_at(v, j, x, 0, guard)) {
+      const long long st = next_start_from(v, j, 0, guard);
+      return st == kInf64 ? kInf64 : st - x;
+    }
+    if (step <= 0) return 0;
+    // every point up to the end of gap j's usable interval fits too
+    const long long ue = max(usable_end(v, j, guard), x);
+    const long long ni = (ue - x0) / step + 1;
+    if (ni >= cnt) return 0;
+    i = ni;
+  }
+}
+
 struct ReqGeom {
   long long d0, d1, ovh;
   int extra;
@@ -382,9 +418,14 @@ __device__ __forceinline__ void pipeline_caps(const PackArgs& a, const TlSlot& s
 // (warp-synchronous); `pi < 0` marks an idle group.
 __device__ __forceinline__ long long group_search(const PackArgs& a, const TlSlot& sl,
                                                   long long gb, int pi, long long arrival,
-                                                  const ReqGeom& rg, int gs, long long& iters) {
+                                                  const ReqGeom& rg, int gs, long long& iters,
+                                                  bool zrun) {
+  // zrun: stages k >= extra have zero layers (D > inference_layers), so their
+  // GPUs only ever hold zero-length prefills, which never change where a
+  // zero-length piece fits: those stages are one run checked on the base list
   const int lane = threadIdx.x & 31, gl = lane & (gs - 1);
-  const int S = sl.S, C = sl.C, D = sl.D;
+  const int S = sl.S, C = sl.C;
+  const int D = zrun ? rg.extra : sl.D;  // stages searched one by one
   const int pipe = pi >= 0 ? pi / S : 0, stage = pi >= 0 ? pi % S : 0;
   const int li = (sl.Ce > 1 ? pipe : 0) * S + stage;
   long long t = pi >= 0 ? arrival : kInf64;
@@ -424,6 +465,11 @@ __device__ __forceinline__ long long group_search(const PackArgs& a, const TlSlo
           prop = st == kInf64 ? kInf64 : max(prop, st - off);
         }
       }
+      if (zrun && gl == (D & (gs - 1)) && prop != kInf64) {  // the zero-length run
+        const long long sh = zero_run_shift(base_view(a, sl, li), t + rg.off(D), rg.ovh,
+                                            sl.D - D, a.guard_ns);
+        prop = sh == kInf64 ? kInf64 : max(prop, t + sh);
+      }
     }
     for (int o = gs >> 1; o > 0; o >>= 1) prop = max(prop, __shfl_xor_sync(kFull, prop, o));
     if (active) {
@@ -444,9 +490,10 @@ __device__ __forceinline__ long long group_search(const PackArgs& a, const TlSlo
 // stages (see pipeline_caps); every lane of the group gets the result.
 __device__ __forceinline__ void group_caps(const PackArgs& a, const TlSlot& sl, long long gb,
                                            int pi, long long a_ref, int extra, int gs,
-                                           long long& capA, long long& capB) {
+                                           long long& capA, long long& capB, bool zrun) {
   const int lane = threadIdx.x & 31, gl = lane & (gs - 1);
-  const int S = sl.S, C = sl.C, D = sl.D;
+  const int S = sl.S, C = sl.C;
+  const int D = zrun ? extra : sl.D;
   const int pipe = pi >= 0 ? pi / S : 0, stage = pi >= 0 ? pi % S : 0;
   const int li = (sl.Ce > 1 ? pipe : 0) * S + stage;
   capA = kInf64;
@@ -457,6 +504,8 @@ __device__ __forceinline__ void group_caps(const PackArgs& a, const TlSlot& sl, 
       const long long r = room_after(v, a_ref, a.guard_ns);
       if (k < extra) capA = min(capA, r); else capB = min(capB, r);
     }
+    // zero-length stages: their lists keep the base list's allowed points
+    if (zrun && gl == (D & (gs - 1))) capB = room_after(base_view(a, sl, li), a_ref, a.guard_ns);
   }
   for (int o = gs >> 1; o > 0; o >>= 1) {
     capA = min(capA, __shfl_xor_sync(kFull, capA, o));
@@ -483,8 +532,12 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
   const long long gb = a.gpu_base[si];
   const int G = D * C * S;
   const int n_pipes = C * S;
+  // build_prefill_pipelines (bubbletea.cpp:88-130): layers per cell
+  const int base_l = a.inf_layers / D, extra = a.inf_layers % D;
+  const bool zrun = base_l == 0;  // stages >= extra carry no layers
+  const int d_eff = zrun ? extra + 1 : D;  // searched stages (+ the zero-length run)
   int gs = 1;
-  while (gs < D && gs < 32) gs <<= 1;
+  while (gs < d_eff && gs < 32) gs <<= 1;
   const int ng = 32 / gs, grp = lane / gs, gl = lane & (gs - 1);
   unsigned* memo = a.memo + (size_t)si * a.max_pipes * a.memo_words;
   long long* capA = pk_smem + (size_t)warp * 2 * a.max_pipes;
@@ -493,8 +546,6 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
   __syncwarp();
   const long long pool_base = (long long)si * a.pool_per_slot;
   long long bump = 0;
-  // build_prefill_pipelines (bubbletea.cpp:88-130): layers per cell
-  const int base_l = a.inf_layers / D, extra = a.inf_layers % D;
   const int total_layers = max(1, base_l * D + extra);
   long long accepted = 0;
   unsigned long long hash = 1469598103934665603ull;
@@ -506,7 +557,7 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
   for (int p0 = 0; p0 < n_pipes; p0 += ng) {
     const int pi = p0 + grp < n_pipes ? p0 + grp : -1;
     long long ca, cb;
-    group_caps(a, sl, gb, pi, a0, extra, gs, ca, cb);
+    group_caps(a, sl, gb, pi, a0, extra, gs, ca, cb, zrun);
     if (pi >= 0 && gl == 0) {
       capA[pi] = ca;
       capB[pi] = cb;
@@ -573,7 +624,7 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
           const int pi = bit < 32 ? c0 + (int)bit : -1;
           st_search += pi >= 0 && gl == 0;
           long long tc = clock64();
-          const long long t = group_search(a, sl, gb, pi, arr, g2, gs, st_iter);
+          const long long t = group_search(a, sl, gb, pi, arr, g2, gs, st_iter, zrun);
           st_cyc_search += clock64() - tc;
           tc = clock64();
           const unsigned ok = __ballot_sync(kFull, gl == 0 && pi >= 0 && t != kInf64);
@@ -591,7 +642,7 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
             memo[(size_t)pi * a.memo_words + (tok >> 5)] |= 1u << (tok & 31);
           if (__any_sync(kFull, failed)) {
             long long ca, cb;
-            group_caps(a, sl, gb, failed ? pi : -1, a_ref, extra, gs, ca, cb);
+            group_caps(a, sl, gb, failed ? pi : -1, a_ref, extra, gs, ca, cb, zrun);
             if (failed && gl == 0) {
               capA[pi] = ca;
               capB[pi] = cb;
@@ -610,12 +661,16 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
         const int pipe = win / S, stage = win % S;
         const int li = (Ce > 1 ? pipe : 0) * S + stage;
         bool ovf = false;
-        for (int k0 = 0; k0 < D && !ovf; k0 += 32) {
+        // (zero-length stages of a zrun plan only split gaps: no effect on
+        // any later search, on the gap sums or on the summaries; skipped)
+        const int D_commit = zrun ? extra : D;
+        for (int k0 = 0; k0 < D_commit && !ovf; k0 += 32) {
           const int k = k0 + lane;
-          const int gi = k < D ? gpu_index(k, pipe, stage, C, S) : 0;
-          const long long lo = k < D ? win_t + g2.off(k) : 0, hi = k < D ? lo + g2.dur(k) : 0;
+          const int gi = k < D_commit ? gpu_index(k, pipe, stage, C, S) : 0;
+          const long long lo = k < D_commit ? win_t + g2.off(k) : 0,
+                          hi = k < D_commit ? lo + g2.dur(k) : 0;
           int j = -1, need = 0, ncap = 0, n = 0;
-          if (k < D) {
+          if (k < D_commit) {
             const ListView v0 = view_of(a, sl, gb, gi, li);
             j = fitting_gap(v0, lo, hi - lo, a.guard_ns);
             // a zero-length interval at a gap end changes nothing (upper_bound
@@ -704,7 +759,7 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
         won |= 1u << src;
         {  // the winner's GPU lists changed: its caps now
           long long ca, cb;
-          group_caps(a, sl, gb, grp == 0 ? win : -1, a_ref, extra, gs, ca, cb);
+          group_caps(a, sl, gb, grp == 0 ? win : -1, a_ref, extra, gs, ca, cb, zrun);
           if (lane == 0) {
             capA[win] = ca;
             capB[win] = cb;

@@ -164,3 +164,39 @@ def test_pack_config2_top_plans_long_trace(planner, checker):
         for a, b in zip(gpl[k * n:(k + 1) * n], wpl):
             assert (a.accepted, a.pipeline, a.start_ns, a.ttft_overhead_ms) == \
                 (b.accepted, b.pipeline, b.start_ns, b.ttft_overhead_ms)
+
+
+def test_pack_many_cells_zero_layer_stages(planner, checker):
+    """Plans with more cells than inference layers (D > 8): the trailing
+    stages of every prefill pipeline carry zero layers and zero-length pieces
+    (the touching-gap rule); placements bit-exact on a saturating stream and a
+    synthetic trace."""
+    from paper_2411_14458_b200 import workloads
+    topos, scens = workloads.config2(3_000, seed=5)
+    tarr = abi.array(abi.Topology, topos)
+    planner.load(tarr, abi.array(abi.Scenario, scens))
+    planner.evaluate()
+    rows = planner.rows()
+    cand = sorted(((r.throughput, i) for i, r in enumerate(rows[:planner.n_rows])
+                   if r.feasible == 1 and 9 <= r.d <= 70), key=lambda x: (-x[0], x[1]))
+    top = [i for _, i in cand[:3]]
+    assert top
+    for guard in (0.0, 0.5):
+        pm = abi.PrefillModel.default(guard_ms=guard)
+        hmax = max(rows[i].makespan_ns for i in top) / 1e6
+        reqs = list(synthetic_requests(300, 11, hmax, pm))
+        got, gpl = planner.pack_prefills(top, reqs, pm, placements=True)
+        n = len(reqs)
+        for k, i in enumerate(top):
+            sc = scens[rows[i].scenario]
+            want, wpl = checker.pack(tarr, sc, rows[i].d, reqs, pm)
+            g = got[k]
+            assert (g.accepted, g.placement_hash, g.utilization_after) == \
+                (want.accepted, want.placement_hash, want.utilization_after), (k, guard)
+            for a, b in zip(gpl[k * n:(k + 1) * n], wpl):
+                assert (a.accepted, a.pipeline, a.start_ns) == (b.accepted, b.pipeline, b.start_ns)
+        sat = checker.saturating(tarr, scens[rows[top[0]].scenario], rows[top[0]].d, pm)[:400]
+        got, _ = planner.pack_prefills([top[0]], sat, pm)
+        want, _ = checker.pack(tarr, scens[rows[top[0]].scenario], rows[top[0]].d, sat, pm,
+                               placements=False)
+        assert (got[0].accepted, got[0].placement_hash) == (want.accepted, want.placement_hash)
