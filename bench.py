@@ -243,7 +243,7 @@ def algorithmic_ops(scens, rows):
 
 # ------------------------------------------------------------- BubbleTea
 
-BT_PLANS, BT_REQS, BT_SEED = 1000, 1000, 42
+BT_PLANS, BT_REQS, BT_SEED = 1000, 10_000, 42
 
 
 def bt_workload(rank, world):

@@ -1213,7 +1213,8 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
   long long pool = 4096;
   for (int i = 0; i < n_rows_sel; ++i) {
     const long long G = (long long)slots[i].D * slots[i].C * slots[i].S;
-    pool = std::max(pool, 3 * (G * (2LL * slots[i].M + 9) + (long long)slots[i].D * n_req));
+    pool = std::max(pool, 3 * (G * (2LL * slots[i].M + 9) +
+                               (long long)slots[i].D * std::min<long long>(n_req, 2048)));
   }
   for (int attempt = 0; attempt < 8; ++attempt) {
     long long* pool_lo = (long long*)c.dev_buf(c.b_tl_scratch, 17 * (size_t)pool * std::max(1, n_rows_sel));
