@@ -441,6 +441,33 @@ __device__ __forceinline__ long long group_search(const PackArgs& a, const TlSlo
     const int k = gl + p * gs;
     if (active && k < D) vv[p] = view_of(a, sl, gb, gpu_index(k, pipe, stage, C, S), li);
   }
+  // Latest feasible start: piece k must end inside the last gap that can hold
+  // it, so t <= usable_end - dur_k - off_k of that gap (the zero-length run:
+  // its last point at or before the last usable end). A search fails as soon
+  // as t passes the group minimum.
+  long long lim = kInf64;
+  if (active) {
+    for (int k = gl; k < D; k += gs) {
+      const ListView v = k < gl + kP * gs ? vv[(k - gl) / gs] :
+                         view_of(a, sl, gb, gpu_index(k, pipe, stage, C, S), li);
+      const long long dk = rg.dur(k);
+      int j = v.n - 1;
+      while (j >= 0 && usable_end(v, j, a.guard_ns) - v.lo[j] < dk) --j;
+      lim = min(lim, j < 0 ? -kInf64 : usable_end(v, j, a.guard_ns) - dk - rg.off(k));
+    }
+    if (zrun && gl == (D & (gs - 1))) {
+      const ListView v = base_view(a, sl, li);
+      long long ue = -kInf64;
+      for (int j = v.n - 1; j >= 0 && ue == -kInf64; --j)
+        if (usable_end(v, j, a.guard_ns) >= v.lo[j]) ue = usable_end(v, j, a.guard_ns);
+      lim = min(lim, ue == -kInf64 ? -kInf64 : ue - rg.off(sl.D - 1));
+    }
+  }
+  for (int o = gs >> 1; o > 0; o >>= 1) lim = min(lim, __shfl_xor_sync(kFull, lim, o));
+  if (active && t > lim) {
+    t = kInf64;
+    active = false;
+  }
   while (__any_sync(kFull, active)) {
     ++iters;
     long long prop = t;
@@ -473,7 +500,7 @@ __device__ __forceinline__ long long group_search(const PackArgs& a, const TlSlo
     }
     for (int o = gs >> 1; o > 0; o >>= 1) prop = max(prop, __shfl_xor_sync(kFull, prop, o));
     if (active) {
-      if (prop == kInf64) {
+      if (prop == kInf64 || prop > lim) {
         t = kInf64;
         active = false;
       } else if (prop == t) {
