@@ -236,9 +236,14 @@ template <int B, bool TIMELINE>
 __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L, AtlasMem& X,
                                               long long (&gfr)[B], int (&drr)[B],
                                               const int (&wbi)[B], const long long (&serb)[B],
-                                              const long long (&latb)[B], long long& n_pairs,
+                                              const long long (&latb)[B],
+                                              long long (&ownb)[B], int (&mcur)[B],
+                                              const int (&mn)[B], long long& n_pairs,
                                               long long& n_scans, long long& n_rounds,
                                               long long* cph) {
+  // ownb[j]: start of pipeline p's last reservation on stage j's gradient
+  // link (its own list tail); mcur/mn: cursor into / size of the link's
+  // static merged list — register copies, one lane owns each stage
   long long ct = cph ? clock64() : 0;
   const int lane = threadIdx.x & 31;
   const int S = g.S, M = g.M, C = g.C;
@@ -264,7 +269,7 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
     nmax = max(nmax, cnt[j]);
   }
   const int R = __reduce_max_sync(kFull, nmax);
-  {
+  if (cph) {
     int tot = 0;
 #pragma unroll
     for (int j = 0; j < B; ++j) tot += cnt[j];
@@ -343,10 +348,7 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
         const int w = wbi[j];
         if (w >= 0 && conf < 0) {
           const long long y = lo[j] + dur + dl[j];
-          const int k = drr[j] + r;
-          const long long own = k > 0 ? X.resb[((size_t)w * C + p) * M + k - 1] : kNegMP;
-          if (link_conflict(X.mb + (size_t)w * C * M, X.mcnt[8 + w], X.mcnt[16 + w], own,
-                            serb[j], y)) {
+          if (link_conflict(X.mb + (size_t)w * C * M, mn[j], mcur[j], ownb[j], serb[j], y)) {
             conf = j;
             conf_y = y;
           }
@@ -356,14 +358,11 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
       if (!bal) break;
       const int src = 31 - __clz(bal);  // topmost conflict: its input is final
       if (lane == src) {
-        const int w = wbi[conf];
-        const int k = drr[conf] + r;
-        const long long own = k > 0 ? X.resb[((size_t)w * C + p) * M + k - 1] : kNegMP;
-        const long long fit = link_fit(X.mb + (size_t)w * C * M, X.mcnt[8 + w], X.mcnt[16 + w],
-                                       own, serb[conf], conf_y);
 #pragma unroll
         for (int j = 0; j < B; ++j)
-          if (j == conf) dl[j] += fit - conf_y;
+          if (j == conf)
+            dl[j] += link_fit(X.mb + (size_t)wbi[j] * C * M, mn[j], mcur[j], ownb[j], serb[j],
+                              conf_y) - conf_y;
       }
     }
     if (cph) {
@@ -380,7 +379,10 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
       const long long t = lo[j] + dl[j];
       const long long e = t + dur;
       gfr[j] = e;
-      if (wbi[j] >= 0) X.resb[((size_t)wbi[j] * C + p) * M + k] = e;  // reserve
+      if (wbi[j] >= 0) {  // reserve (append to list p)
+        X.resb[((size_t)wbi[j] * C + p) * M + k] = e;
+        ownb[j] = e;
+      }
       if (s > 0) X.garr[((size_t)p * S + s - 1) * M + k] = e + wl[j];
       if (TIMELINE) X.ps[((size_t)p * S + s) * M + k] = t;
     }
@@ -642,9 +644,25 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
         __syncwarp();
       }
     }
-    if (lane < 8) X.mcnt[16 + lane] = 0;
     curf = 0;
     __syncwarp();
+    long long ownb[B];
+    int mcur[B], mn[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      ownb[j] = kNegMP;
+      mcur[j] = 0;
+      mn[j] = wbi[j] >= 0 ? X.mcnt[8 + wbi[j]] : 0;
+    }
+    // lane w < nw: link w's constants for this pipeline (chain checks)
+    long long aw_l = 0, lenw_l = 0, ownw_l = kNegMP;
+    const long long* mgw_l = nullptr;
+    int nmw_l = 0;
+    if (lane < nw) {
+      lenw_l = X.wa[8 + lane];
+      mgw_l = X.mf + (size_t)lane * C * M;
+      nmw_l = X.mcnt[lane];
+    }
     for (int m = 0; m < M; ++m) {
       // memory-cap admission (:366-381) + forced drains (:321-346)
       if (phase) ph_t = clock64();
@@ -655,8 +673,8 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
 #pragma unroll
       nblk = __reduce_add_sync(kFull, nblk);
       if (nblk > 0) {
-        atlas_cascade<B, TIMELINE>(g, p, m, mem_limit, X, gfr, drr, wbi, serb, latb, n_pairs,
-                                   n_stage_it, n_rounds, phase ? cph : nullptr);
+        atlas_cascade<B, TIMELINE>(g, p, m, mem_limit, X, gfr, drr, wbi, serb, latb, ownb, mcur,
+                                   mn, n_pairs, n_stage_it, n_rounds, phase ? cph : nullptr);
         ++n_adm;
       }
       if (phase) {
@@ -699,28 +717,25 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
       // (lane w checks link w; the lowest conflicting link shifts t0, as the
       // reference's restart from stage 0 does)
       if (nw > 0) {
-        long long aw = 0, gw = 0, lenw = 0, ownw = kNegMP;
-        const long long* mgw = nullptr;
-        int nmw = 0;
+        long long gw = 0;
         if (lane < nw) {
-          aw = X.wa[lane];
+          aw_l = X.wa[lane];
           gw = X.wg[lane];
-          lenw = X.wa[8 + lane];
-          mgw = X.mf + (size_t)lane * C * M;
-          nmw = X.mcnt[lane];
-          if (m > 0) ownw = X.resf[((size_t)lane * C + p) * M + m - 1];
         }
         for (;;) {
-          const long long e = aw + f + imax(t0, gw);
-          const bool conf = lane < nw && link_conflict(mgw, nmw, curf, ownw, lenw, e);
+          const long long e = aw_l + f + imax(t0, gw);
+          const bool conf = lane < nw && link_conflict(mgw_l, nmw_l, curf, ownw_l, lenw_l, e);
           const unsigned bal = __ballot_sync(kFull, conf);
           if (!bal) break;
           const int src = __ffs(bal) - 1;
           long long shift = 0;
-          if (lane == src) shift = link_fit(mgw, nmw, curf, ownw, lenw, e) - e;
+          if (lane == src) shift = link_fit(mgw_l, nmw_l, curf, ownw_l, lenw_l, e) - e;
           t0 += shfl_idx64(shift, src);
         }
-        if (lane < nw) X.resf[((size_t)lane * C + p) * M + m] = aw + f + imax(t0, gw);
+        if (lane < nw) {
+          ownw_l = aw_l + f + imax(t0, gw);
+          X.resf[((size_t)lane * C + p) * M + m] = ownw_l;
+        }
       }
       if (phase) {
         const long long t1 = clock64();
