@@ -18,7 +18,7 @@ struct AtlasLayout {
   size_t off_wa, off_wg, off_wbs, off_gf, off_nm, off_firstm, off_mcnt, off_big, off_garr,
       total;
   // "big" region (lists), relative to its base
-  size_t off_fdl, off_resf, off_resb, off_mf, off_mb, off_mtmp, big_total;
+  size_t off_fdl, off_resf, off_resb, off_mf, off_mb, off_mtmp, off_jf, off_jb, big_total;
   int cap;             // list storage per WAN boundary = C * M (C lists of M)
 
   __host__ __device__ static size_t al(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -34,6 +34,8 @@ struct AtlasLayout {
     off_mf = o;        o = al(o + (size_t)nw * cap * 8);
     off_mb = o;        o = al(o + (size_t)nw * cap * 8);
     off_mtmp = o;      o = al(o + (size_t)cap * 8);
+    off_jf = o;        o = al(o + (size_t)nw * cap * 4);  // run jumps of mf / mb
+    off_jb = o;        o = al(o + (size_t)nw * cap * 4);
     big_total = o;
     o = 0;
     off_wa = o;        o = al(o + 16 * 8);          // a_w [0,8) | ser_w [8,16)

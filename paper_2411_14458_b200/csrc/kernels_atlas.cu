@@ -89,6 +89,7 @@ struct AtlasMem {
   long long garr_cap;
   int *wbs, *nm, *firstm;
   long long *mf, *mb, *mtmp;  // merged static link lists (forward phase)
+  int *jf, *jb;               // their run jumps
   int* mcnt;                  // [w] |mf|, [8+w] |mb|, [16+w] mb cursor
   long long* fe;  // timeline: forward ends [C][S][M] (global)
   long long* ps;  // timeline: pair starts  [C][S][M] (global)
@@ -111,6 +112,8 @@ struct AtlasMem {
     mf = (long long*)(big + L.off_mf);
     mb = (long long*)(big + L.off_mb);
     mtmp = (long long*)(big + L.off_mtmp);
+    jf = (int*)(big + L.off_jf);
+    jb = (int*)(big + L.off_jb);
     garr_smem = (long long*)(base + L.off_garr);
     garr_glob = garr_global;
     garr_cap = L.garr_cap;
@@ -172,6 +175,25 @@ __device__ __forceinline__ void link_advance(const long long* mg, int n, int& cu
   cur = lo;
 }
 
+// Run jumps of a static list whose intervals all have length len:
+// jmp[i] = the first j >= i after which a free gap of at least len opens
+// (mg[j+1] - (mg[j] + len) >= len, or j = n-1). earliest_fit that overlaps
+// entry i lands exactly at mg[jmp[i]] + len. Warp-parallel from the tail,
+// 32 entries per step.
+__device__ __forceinline__ void warp_jumps(const long long* mg, int n, long long len, int* jmp) {
+  const int lane = threadIdx.x & 31;
+  int carry = n - 1;  // first flagged index of the part already done
+  for (int base = ((n - 1) >> 5) << 5; base >= 0 && n > 0; base -= 32) {
+    const int i = base + lane;
+    const bool flag = i < n && (i == n - 1 || mg[i + 1] - mg[i] - len >= len);
+    const unsigned fm = __ballot_sync(kFull, flag) & (0xffffffffu << lane);
+    if (i < n) jmp[i] = fm ? base + __ffs(fm) - 1 : carry;
+    const unsigned all = __ballot_sync(kFull, flag);
+    if (all) carry = base + __ffs(all) - 1;
+  }
+  __syncwarp();
+}
+
 // [x, x+len) overlaps a static entry (cursor `cur`, advanced) or the own tail
 __device__ __forceinline__ bool link_conflict(const long long* mg, int n, int& cur,
                                               long long own_last, long long len, long long x) {
@@ -181,15 +203,18 @@ __device__ __forceinline__ bool link_conflict(const long long* mg, int n, int& c
   return own_last + len > x;
 }
 
-// earliest_fit over the static list and the own tail
-__device__ __forceinline__ long long link_fit(const long long* mg, int n, int& cur,
+// earliest_fit over the static list and the own tail; a run of back-to-back
+// static entries is crossed in one step through the jump table
+__device__ __forceinline__ long long link_fit(const long long* mg, const int* jmp, int n, int& cur,
                                               long long own_last, long long len, long long x) {
   if (len <= 0) return x;
   long long t = x;
   for (;;) {
     link_advance(mg, n, cur, len, t);
     if (cur < n && mg[cur] < t + len) {
+      cur = jmp[cur];
       t = mg[cur] + len;
+      ++cur;
       continue;
     }
     if (own_last + len > t) {
@@ -325,7 +350,8 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
       }
       // inclusive suffix scan over the nl stage-owning lanes (higher lanes =
       // deeper stages first)
-      for (int o = 1; o < nl; o <<= 1) {
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {  // fixed trip count: no divergent shuffles
         const long long oa = shfl_down64(ta, o), ob = shfl_down64(tb, o);
         if (lane + o < nl) {
           tb = imax(mp_add(ob, ta), tb);
@@ -361,7 +387,8 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
 #pragma unroll
         for (int j = 0; j < B; ++j)
           if (j == conf)
-            dl[j] += link_fit(X.mb + (size_t)wbi[j] * C * M, mn[j], mcur[j], ownb[j], serb[j],
+            dl[j] += link_fit(X.mb + (size_t)wbi[j] * C * M, X.jb + (size_t)wbi[j] * C * M, mn[j],
+                              mcur[j], ownb[j], serb[j],
                               conf_y) - conf_y;
       }
     }
@@ -508,6 +535,7 @@ __device__ void drain_stage_greedy(const Geom& g, AtlasMem& X, int s, int w) {
   const int S = g.S, M = g.M, C = g.C;
   const long long dur = g.dur, len = g.ser_pooled[w], wl = g.ser_pooled[w] + g.lat[w];
   const long long* mg = X.mb + (size_t)w * C * M;
+  const int* jg = X.jb + (size_t)w * C * M;
   const int nmg = X.mcnt[8 + w];
   int mq = q < C ? X.nm[q * S + s] : M;
   long long gfq = q < C ? X.gf[q * S + s] : 0;
@@ -515,7 +543,7 @@ __device__ void drain_stage_greedy(const Geom& g, AtlasMem& X, int s, int w) {
   long long last_a = kNegMP;  // start of this stage's last committed transfer
   auto fresh = [&]() -> long long {
     const long long r = s == S - 1 ? X.fdl[q * M + mq] : X.garr[((size_t)q * S + s) * M + mq];
-    return link_fit(mg, nmg, cur, last_a, len, imax(r, gfq) + dur) - dur;
+    return link_fit(mg, jg, nmg, cur, last_a, len, imax(r, gfq) + dur) - dur;
   };
   long long cand = mq < M ? fresh() : kInf64;
   for (;;) {
@@ -543,7 +571,7 @@ __device__ void drain_stage_greedy(const Geom& g, AtlasMem& X, int s, int w) {
     if (q == bq) {
       cand = mq < M ? fresh() : kInf64;
     } else if (cand != kInf64 && cand + dur < last_a + len) {
-      cand = link_fit(mg, nmg, cur, last_a, len, cand + dur) - dur;  // pushed by the commit
+      cand = link_fit(mg, jg, nmg, cur, last_a, len, cand + dur) - dur;  // pushed by the commit
     }
   }
   if (q < C) {
@@ -637,6 +665,9 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
         warp_merge(X.mf + (size_t)w * C * M, nf, X.resf + ((size_t)w * C + p - 1) * M, M, X.mtmp);
         warp_merge(X.mb + (size_t)w * C * M, nbk, X.resb + ((size_t)w * C + p - 1) * M, add_b,
                    X.mtmp);
+        warp_jumps(X.mf + (size_t)w * C * M, nf + M, g.ser_pooled[w], X.jf + (size_t)w * C * M);
+        warp_jumps(X.mb + (size_t)w * C * M, nbk + add_b, g.ser_pooled[w],
+                   X.jb + (size_t)w * C * M);
         if (lane == 0) {
           X.mcnt[w] = nf + M;
           X.mcnt[8 + w] = nbk + add_b;
@@ -657,10 +688,12 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     // lane w < nw: link w's constants for this pipeline (chain checks)
     long long aw_l = 0, lenw_l = 0, ownw_l = kNegMP;
     const long long* mgw_l = nullptr;
+    const int* jgw_l = nullptr;
     int nmw_l = 0;
     if (lane < nw) {
       lenw_l = X.wa[8 + lane];
       mgw_l = X.mf + (size_t)lane * C * M;
+      jgw_l = X.jf + (size_t)lane * C * M;
       nmw_l = X.mcnt[lane];
     }
     for (int m = 0; m < M; ++m) {
@@ -691,7 +724,8 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
         gl[j] = runmax;
       }
       long long pre = runmax;
-      for (int o = 1; o < nl; o <<= 1) {
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
         const long long v = shfl_up64(pre, o);
         if (lane >= o) pre = imax(pre, v);
       }
@@ -729,7 +763,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
           if (!bal) break;
           const int src = __ffs(bal) - 1;
           long long shift = 0;
-          if (lane == src) shift = link_fit(mgw_l, nmw_l, curf, ownw_l, lenw_l, e) - e;
+          if (lane == src) shift = link_fit(mgw_l, jgw_l, nmw_l, curf, ownw_l, lenw_l, e) - e;
           t0 += shfl_idx64(shift, src);
         }
         if (lane < nw) {
@@ -775,6 +809,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     const int nbk = X.mcnt[8 + w], add_b = X.nm[(C - 1) * S + sw];
     warp_merge(X.mb + (size_t)w * C * M, nbk, X.resb + ((size_t)w * C + C - 1) * M, add_b,
                X.mtmp);
+    warp_jumps(X.mb + (size_t)w * C * M, nbk + add_b, g.ser_pooled[w], X.jb + (size_t)w * C * M);
     if (lane == 0) X.mcnt[8 + w] = nbk + add_b;
     __syncwarp();
   }
