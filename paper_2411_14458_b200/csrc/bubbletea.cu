@@ -415,7 +415,9 @@ __device__ __forceinline__ void pipeline_caps(const PackArgs& a, const TlSlot& s
 // feasible start lies below any proposal). The fixpoint is the earliest
 // common start t0 >= arrival, the minimum of the reference's candidate set
 // (bubbletea.cpp:164-188), or kInf64. Every lane of the warp must call it
-// (warp-synchronous); `pi < 0` marks an idle group.
+// (warp-synchronous); `pi < 0` marks an idle group. The lane's first kP
+// stages keep their list view and search cursor in registers.
+template <int kP>
 __device__ __forceinline__ long long group_search(const PackArgs& a, const TlSlot& sl,
                                                   long long gb, int pi, long long arrival,
                                                   const ReqGeom& rg, int gs, long long& iters,
@@ -430,9 +432,7 @@ __device__ __forceinline__ long long group_search(const PackArgs& a, const TlSlo
   const int li = (sl.Ce > 1 ? pipe : 0) * S + stage;
   long long t = pi >= 0 ? arrival : kInf64;
   bool active = pi >= 0;
-  // the lane's first kP stages keep their list view and search cursor in
-  // registers for the whole search (t only grows; the lists do not change)
-  constexpr int kP = 4;
+  // (t only grows during a search and the lists do not change)
   ListView vv[kP];
   int cur[kP];
 #pragma unroll
@@ -446,15 +446,18 @@ __device__ __forceinline__ long long group_search(const PackArgs& a, const TlSlo
   // its last point at or before the last usable end). A search fails as soon
   // as t passes the group minimum.
   long long lim = kInf64;
+  auto stage_lim = [&](const ListView& v, int k) {
+    const long long dk = rg.dur(k);
+    int j = v.n - 1;
+    while (j >= 0 && usable_end(v, j, a.guard_ns) - v.lo[j] < dk) --j;
+    return j < 0 ? -kInf64 : usable_end(v, j, a.guard_ns) - dk - rg.off(k);
+  };
   if (active) {
-    for (int k = gl; k < D; k += gs) {
-      const ListView v = k < gl + kP * gs ? vv[(k - gl) / gs] :
-                         view_of(a, sl, gb, gpu_index(k, pipe, stage, C, S), li);
-      const long long dk = rg.dur(k);
-      int j = v.n - 1;
-      while (j >= 0 && usable_end(v, j, a.guard_ns) - v.lo[j] < dk) --j;
-      lim = min(lim, j < 0 ? -kInf64 : usable_end(v, j, a.guard_ns) - dk - rg.off(k));
-    }
+#pragma unroll
+    for (int p = 0; p < kP; ++p)
+      if (gl + p * gs < D) lim = min(lim, stage_lim(vv[p], gl + p * gs));
+    for (int k = gl + kP * gs; k < D; k += gs)
+      lim = min(lim, stage_lim(view_of(a, sl, gb, gpu_index(k, pipe, stage, C, S), li), k));
     if (zrun && gl == (D & (gs - 1))) {
       const ListView v = base_view(a, sl, li);
       long long ue = -kInf64;
@@ -569,6 +572,9 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
   unsigned* memo = a.memo + (size_t)si * a.max_pipes * a.memo_words;
   long long* capA = pk_smem + (size_t)warp * 2 * a.max_pipes;
   long long* capB = capA + a.max_pipes;
+  // per-batch "committed" flag per pipeline
+  unsigned char* cflag = (unsigned char*)(pk_smem + (size_t)(blockDim.x >> 5) * 2 * a.max_pipes) +
+                         (size_t)warp * a.max_pipes;
   for (int i = lane; i < G; i += 32) a.gpu_off[gb + i] = -1;
   __syncwarp();
   const long long pool_base = (long long)si * a.pool_per_slot;
@@ -622,62 +628,112 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
       }
     }
     const bool in_range = r < a.n_req;
-    unsigned todo = __ballot_sync(kFull, live && rg.d0 <= mB && (extra == 0 || rg.d1 <= mA));
+    const unsigned todo0 = __ballot_sync(kFull, live && rg.d0 <= mB && (extra == 0 || rg.d1 <= mA));
     unsigned won = 0;
     long long my_start = -1;
     int my_pipe = -1;
-    while (todo) {
+    // Phase 1 — every staged request searches the batch-start state at once
+    // (lane = request, pipelines in order, its stages checked with independent
+    // loads). Commits only shrink gap lists and only on the committing
+    // pipeline's own GPUs, so a pipeline infeasible at the batch start stays
+    // infeasible for the rest of the batch, and a request's answer (pipeline,
+    // earliest start) stays exact unless an earlier request of the batch
+    // committed to that same pipeline (phase 2 re-searches those).
+    const bool act = (todo0 >> lane) & 1u;
+    const int tok_l = q.tokens - 1;
+    int pi_l = act ? 0 : n_pipes;
+    int pipe1 = -1;
+    long long t1 = kInf64;
+    unsigned long long failm = 0;  // pipelines < 64 that failed this lane's search
+    {
+      const long long tc = clock64();
+      for (;;) {
+        int cand = -1;
+        for (; pi_l < n_pipes; ++pi_l) {
+          if (rg.d0 <= capB[pi_l] && (extra == 0 || rg.d1 <= capA[pi_l]) &&
+              !((memo[(size_t)pi_l * a.memo_words + (tok_l >> 5)] >> (tok_l & 31)) & 1u)) {
+            cand = pi_l;
+            break;
+          }
+        }
+        if (!__any_sync(kFull, cand >= 0)) break;
+        st_search += cand >= 0;
+        const long long t = group_search<8>(a, sl, gb, cand, arrival, rg, 1, st_iter, zrun);
+        if (cand >= 0) {
+          if (t != kInf64) {
+            pipe1 = cand;
+            t1 = t;
+            pi_l = n_pipes;
+          } else {
+            ++st_fail;
+            if (cand < 64) failm |= 1ull << cand;
+            ++pi_l;
+          }
+        }
+      }
+      st_cyc_search += clock64() - tc;
+    }
+    for (int i = lane; i < n_pipes; i += 32) cflag[i] = 0;
+    __syncwarp();
+    // Phase 2 — FCFS over the batch: commit each answer whose pipeline no
+    // earlier request of the batch took; otherwise search again from that
+    // pipeline on (warp-cooperative, lane groups over pipelines).
+    unsigned res = __ballot_sync(kFull, pipe1 >= 0);
+    while (res) {
       ++st_exam;
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const long long arr = shfl_idx64(arrival, src);
+      const int src = __ffs(res) - 1;
+      res &= res - 1;
+      int win = __shfl_sync(kFull, pipe1, src);
+      long long win_t = shfl_idx64(t1, src);
       const long long a_ref = a.sufmin[r0 + src];  // <= every arrival from here on
       ReqGeom g2;
       g2.d0 = shfl_idx64(rg.d0, src);
       g2.d1 = shfl_idx64(rg.d1, src);
       g2.ovh = shfl_idx64(rg.ovh, src);
       g2.extra = extra;
-      const int tok = __shfl_sync(kFull, q.tokens, src) - 1;
-      int win = -1;
-      long long win_t = 0;
-      for (int c0 = 0; c0 < n_pipes && win < 0; c0 += 32) {
-        const int pl = c0 + lane;
-        bool cand = pl < n_pipes && g2.d0 <= capB[pl] && (extra == 0 || g2.d1 <= capA[pl]);
-        if (cand) cand = !((memo[(size_t)pl * a.memo_words + (tok >> 5)] >> (tok & 31)) & 1u);
-        unsigned pmask = __ballot_sync(kFull, cand);
-        while (pmask && win < 0) {
-          // the next ng survivors, in pipeline order, one per group
-          const unsigned bit = __fns(pmask, 0, grp + 1);
-          const int pi = bit < 32 ? c0 + (int)bit : -1;
-          st_search += pi >= 0 && gl == 0;
-          long long tc = clock64();
-          const long long t = group_search(a, sl, gb, pi, arr, g2, gs, st_iter, zrun);
-          st_cyc_search += clock64() - tc;
-          tc = clock64();
-          const unsigned ok = __ballot_sync(kFull, gl == 0 && pi >= 0 && t != kInf64);
-          if (ok) {
-            const int wl = __ffs(ok) - 1;  // lowest group = lowest pipeline
-            win = __shfl_sync(kFull, pi, wl);
-            win_t = shfl_idx64(t, wl);
-          }
-          // failed searches below the winner (or all): tighten their caps
-          const bool failed = pi >= 0 && t == kInf64 && (win < 0 || pi < win);
-          st_fail += failed && gl == 0;
-          // no start >= arr exists for this token count; every later request
-          // arrives at or after arr when arr is the minimum of the rest
-          if (failed && gl == 0 && arr == a_ref)
-            memo[(size_t)pi * a.memo_words + (tok >> 5)] |= 1u << (tok & 31);
-          if (__any_sync(kFull, failed)) {
-            long long ca, cb;
-            group_caps(a, sl, gb, failed ? pi : -1, a_ref, extra, gs, ca, cb, zrun);
-            if (failed && gl == 0) {
-              capA[pi] = ca;
-              capB[pi] = cb;
+      if (cflag[win]) {
+        const long long tc = clock64();
+        const int from = win;
+        const long long arr = shfl_idx64(arrival, src);
+        const int tok = __shfl_sync(kFull, q.tokens, src) - 1;
+        win = -1;
+        for (int c0 = from & ~31; c0 < n_pipes && win < 0; c0 += 32) {
+          const int pl = c0 + lane;
+          bool cand = pl >= from && pl < n_pipes && g2.d0 <= capB[pl] &&
+                      (extra == 0 || g2.d1 <= capA[pl]);
+          if (cand) cand = !((memo[(size_t)pl * a.memo_words + (tok >> 5)] >> (tok & 31)) & 1u);
+          unsigned pmask = __ballot_sync(kFull, cand);
+          while (pmask && win < 0) {
+            // the next ng survivors, in pipeline order, one per group
+            const unsigned bit = __fns(pmask, 0, grp + 1);
+            const int pi = bit < 32 ? c0 + (int)bit : -1;
+            st_search += pi >= 0 && gl == 0;
+            const long long t = group_search<4>(a, sl, gb, pi, arr, g2, gs, st_iter, zrun);
+            const unsigned ok = __ballot_sync(kFull, gl == 0 && pi >= 0 && t != kInf64);
+            if (ok) {
+              const int wl = __ffs(ok) - 1;  // lowest group = lowest pipeline
+              win = __shfl_sync(kFull, pi, wl);
+              win_t = shfl_idx64(t, wl);
             }
+            // failed searches below the winner (or all): tighten their caps
+            const bool failed = pi >= 0 && t == kInf64 && (win < 0 || pi < win);
+            st_fail += failed && gl == 0;
+            // no start >= arr exists for this token count; every later request
+            // arrives at or after arr when arr is the minimum of the rest
+            if (failed && gl == 0 && arr == a_ref)
+              atomicOr(&memo[(size_t)pi * a.memo_words + (tok >> 5)], 1u << (tok & 31));
+            if (__any_sync(kFull, failed)) {
+              long long ca, cb;
+              group_caps(a, sl, gb, failed ? pi : -1, a_ref, extra, gs, ca, cb, zrun);
+              if (failed && gl == 0) {
+                capA[pi] = ca;
+                capB[pi] = cb;
+              }
+            }
+            for (int g = 0; g < ng && pmask; ++g) pmask &= pmask - 1;
           }
-          st_cyc_caps += clock64() - tc;
-          for (int g = 0; g < ng && pmask; ++g) pmask &= pmask - 1;
         }
+        st_cyc_caps += clock64() - tc;
       }
       __syncwarp();
       const long long tcm = clock64();
@@ -778,6 +834,7 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
           hash = fnv_mix(hash, (unsigned long long)(long long)id);
           hash = fnv_mix(hash, (unsigned long long)(long long)win);
           hash = fnv_mix(hash, (unsigned long long)win_t);
+          cflag[win] = 1;
         }
         if (lane == src) {
           my_pipe = win;
@@ -795,8 +852,37 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
       }
       __syncwarp();
       st_cyc_commit += clock64() - tcm;
-      // caps only shrink: refresh the warp bounds and drop staged requests
-      // they no longer admit
+    }
+    // Phase-1 failures, recorded now that the batch is resolved: the memo
+    // (a failure at the minimum remaining arrival holds for every later
+    // request with that token count) and the failed pipelines' caps at the
+    // next batch's reference time.
+    if (act && failm && arrival == a.sufmin[r]) {
+      for (unsigned long long m = failm; m; m &= m - 1) {
+        const int pi = __ffsll((long long)m) - 1;
+        atomicOr(&memo[(size_t)pi * a.memo_words + (tok_l >> 5)], 1u << (tok_l & 31));
+      }
+    }
+    if (r0 + 32 < a.n_req) {
+      unsigned long long um = failm;
+      for (int o = 16; o > 0; o >>= 1) um |= __shfl_xor_sync(kFull, um, o);
+      const long long a_next = a.sufmin[r0 + 32];
+      while (um) {
+        // the next ng failed pipelines, one per group
+        unsigned long long mm = um;
+        for (int g = 0; g < grp && mm; ++g) mm &= mm - 1;
+        const int pi = mm ? __ffsll((long long)mm) - 1 : -1;
+        long long ca, cb;
+        group_caps(a, sl, gb, pi, a_next, extra, gs, ca, cb, zrun);
+        if (pi >= 0 && gl == 0) {
+          capA[pi] = ca;
+          capB[pi] = cb;
+        }
+        for (int g = 0; g < ng && um; ++g) um &= um - 1;
+      }
+    }
+    __syncwarp();
+    {  // caps only shrink: refresh the warp bounds
       long long ma = -kInf64, mb = -kInf64;
       for (int pi = lane; pi < n_pipes; pi += 32) {
         ma = max(ma, capA[pi]);
@@ -804,7 +890,6 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
       }
       mA = warp_max64(ma);
       mB = warp_max64(mb);
-      todo &= __ballot_sync(kFull, live && rg.d0 <= mB && (extra == 0 || rg.d1 <= mA));
     }
     if (a.pl && in_range) {
       gpb_placement& o = a.pl[(size_t)si * a.n_req + r];
@@ -1284,7 +1369,7 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
     int max_pipes = 1;
     for (const TlSlot& sl2 : slots) max_pipes = std::max(max_pipes, sl2.C * sl2.S);
     a.max_pipes = max_pipes;
-    const size_t psmem = 4 * 2 * sizeof(long long) * (size_t)max_pipes;
+    const size_t psmem = 4 * (2 * sizeof(long long) + 1) * (size_t)max_pipes;
     if (psmem > (size_t)c.smem_optin) {
       c.set_error("too many prefill pipelines per plan for the packing kernel");
       return GPB_CONFIG_ERROR;
