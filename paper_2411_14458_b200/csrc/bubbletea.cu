@@ -32,6 +32,10 @@
 
 namespace gpb {
 
+// Packed gaps (longlong2): x = start, y = end | kGapFl when the next span is a
+// training task (gaps_of's before_training, bubbletea.cpp:48).
+constexpr long long kGapFl = 1LL << 62;
+
 // Per-row descriptor of a timeline / packing slot.
 struct TlSlot {
   long long row;
@@ -86,7 +90,7 @@ __device__ __forceinline__ unsigned long long fnv_mix(unsigned long long h, unsi
 __global__ void gap_kernel(const TlSlot* slots, int n_slots, const long long* fe,
                            const long long* ps, const long long* ar_dur,
                            const long long* ar_start, long long* glo, long long* ghi,
-                           unsigned char* gflag, int* gcnt, long long* gsum, int* ghas,
+                           unsigned char* gflag, longlong2* gpk, int* gcnt, long long* gsum, int* ghas,
                            const long long* hz) {
   // grid.y = slot, threads over its (pipeline, stage) lists
   const int si = blockIdx.y;
@@ -106,6 +110,7 @@ __global__ void gap_kernel(const TlSlot* slots, int n_slots, const long long* fe
   long long* lo_out = glo + sl.gap_off + (size_t)li * (2 * M + 1);
   long long* hi_out = ghi + sl.gap_off + (size_t)li * (2 * M + 1);
   unsigned char* fl_out = gflag + sl.gap_off + (size_t)li * (2 * M + 1);
+  longlong2* pk_out = gpk + sl.gap_off + (size_t)li * (2 * M + 1);
   const bool rev = sl.policy == GPB_GPIPE;  // gpipe drains in reverse order
   int i_f = 0, i_p = 0, n = 0, has = 0;
   long long cursor = 0, sum = 0;
@@ -136,6 +141,7 @@ __global__ void gap_kernel(const TlSlot* slots, int n_slots, const long long* fe
       lo_out[n] = cursor;
       hi_out[n] = lo;
       fl_out[n] = 1;  // the next span is a training task
+      pk_out[n] = make_longlong2(cursor, lo | kGapFl);
       sum += lo - cursor;
       ++n;
     }
@@ -145,6 +151,7 @@ __global__ void gap_kernel(const TlSlot* slots, int n_slots, const long long* fe
     lo_out[n] = cursor;
     hi_out[n] = H;
     fl_out[n] = 0;
+    pk_out[n] = make_longlong2(cursor, H);
     sum += H - cursor;
     ++n;
   }
@@ -161,9 +168,7 @@ struct PackArgs {
   const DevScen* scens;
   const DevTopo* topos;
   const int32_t* row_scen;
-  const long long* glo;
-  const long long* ghi;
-  const unsigned char* gflag;
+  const longlong2* gpk;      // base gap lists, packed (see ListView)
   const int* gcnt;
   const long long* gsum;
   const long long* hz;
@@ -177,9 +182,7 @@ struct PackArgs {
   long long inf_hidden;
   long long guard_ns;
   // copy-on-write per-GPU lists
-  long long* pool_lo;
-  long long* pool_hi;
-  unsigned char* pool_fl;
+  longlong2* pool;
   long long pool_per_slot;
   int max_pipes;              // largest C*S over the slots (shared-memory caps)
   long long* stats;           // nullable: per-slot counters (GPB_PACK_STATS)
@@ -195,27 +198,29 @@ struct PackArgs {
   int* overflow;
 };
 
+// A gap list: 16 bytes per gap (one load), x = start, y = end with the
+// before-training flag in bit 62 (kGapFl).
 struct ListView {
-  const long long* lo;
-  const long long* hi;
-  const unsigned char* fl;
+  const longlong2* e;
   int n;
+  __device__ __forceinline__ long long lo(int j) const { return e[j].x; }
+  __device__ __forceinline__ long long hi(int j) const { return e[j].y & (kGapFl - 1); }
+  __device__ __forceinline__ bool fl(int j) const { return (e[j].y & kGapFl) != 0; }
 };
+__device__ __forceinline__ long long gap_ue(const longlong2& g, long long guard) {
+  return (g.y & (kGapFl - 1)) - ((g.y & kGapFl) ? guard : 0);
+}
 
 __device__ __forceinline__ ListView view_of(const PackArgs& a, const TlSlot& sl, long long gb,
                                             int gi, int li_shared) {
   ListView v;
   const long long off = a.gpu_off[gb + gi];
   if (off >= 0) {
-    v.lo = a.pool_lo + off;
-    v.hi = a.pool_hi + off;
-    v.fl = a.pool_fl + off;
+    v.e = a.pool + off;
     v.n = a.gpu_cnt[gb + gi];
   } else {
     const long long go = sl.gap_off + (long long)li_shared * (2 * sl.M + 1);
-    v.lo = a.glo + go;
-    v.hi = a.ghi + go;
-    v.fl = a.gflag + go;
+    v.e = a.gpk + go;
     v.n = a.gcnt[sl.lst_off + li_shared];
   }
   return v;
@@ -226,13 +231,13 @@ __device__ __forceinline__ int last_start_le(const ListView& v, long long x) {
   int lo = 0, hi = v.n;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (v.lo[mid] <= x) lo = mid + 1; else hi = mid;
+    if (v.lo(mid) <= x) lo = mid + 1; else hi = mid;
   }
   return lo - 1;
 }
 
 __device__ __forceinline__ long long usable_end(const ListView& v, int j, long long guard) {
-  return v.hi[j] - (v.fl[j] ? guard : 0);
+  return gap_ue(v.e[j], guard);
 }
 
 // Gap that admits [lo, lo+dur) in the reference's scan (bubbletea.cpp:173-188):
@@ -243,7 +248,7 @@ __device__ __forceinline__ int fitting_gap(const ListView& v, long long lo, long
   const int j = last_start_le(v, lo);
   if (j < 0) return -1;
   if (lo + dur <= usable_end(v, j, guard)) return j;
-  if (dur == 0 && j >= 1 && v.hi[j - 1] == lo && usable_end(v, j - 1, guard) >= lo) return j - 1;
+  if (dur == 0 && j >= 1 && v.hi(j - 1) == lo && usable_end(v, j - 1, guard) >= lo) return j - 1;
   return -1;
 }
 
@@ -251,9 +256,9 @@ __device__ __forceinline__ int fitting_gap(const ListView& v, long long lo, long
 __device__ __forceinline__ long long next_start(const ListView& v, long long x, long long dur,
                                                 long long guard) {
   for (int j = last_start_le(v, x) + 1; j < v.n; ++j) {
-    const long long st = v.lo[j];
+    const long long st = v.lo(j);
     if (st + dur <= usable_end(v, j, guard)) return st;
-    if (dur == 0 && j >= 1 && v.hi[j - 1] == st && usable_end(v, j - 1, guard) >= st) return st;
+    if (dur == 0 && j >= 1 && v.hi(j - 1) == st && usable_end(v, j - 1, guard) >= st) return st;
   }
   return kInf64;
 }
@@ -267,14 +272,14 @@ __device__ __forceinline__ int last_start_le_from(const ListView& v, long long x
   } else {
     j = c;
     int step = 1;
-    while (j + step < v.n && v.lo[j + step] <= x) {
+    while (j + step < v.n && v.lo(j + step) <= x) {
       j += step;
       step <<= 1;
     }
     int lo = j + 1, hi = min(j + step, v.n);
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (v.lo[mid] <= x) lo = mid + 1; else hi = mid;
+      if (v.lo(mid) <= x) lo = mid + 1; else hi = mid;
     }
     j = lo - 1;
   }
@@ -287,14 +292,57 @@ __device__ __forceinline__ bool fits_at(const ListView& v, int j, long long lo, 
                                         long long guard) {
   if (j < 0) return false;
   if (lo + dur <= usable_end(v, j, guard)) return true;
-  return dur == 0 && j >= 1 && v.hi[j - 1] == lo && usable_end(v, j - 1, guard) >= lo;
+  return dur == 0 && j >= 1 && v.hi(j - 1) == lo && usable_end(v, j - 1, guard) >= lo;
+}
+
+// One stage of a search at x = t + off_k: x itself when [x, x+dur) fits the
+// gap the reference would use (fitting_gap), else the next start that can
+// hold it (next_start, > x), or kInf64. `c` is the search cursor (last gap
+// starting at or before the previous x; < -1: unknown). The common case — x
+// has not passed the next gap's start — costs two independent 16-byte loads.
+__device__ __forceinline__ long long stage_next(const ListView& v, int& c, long long x,
+                                                long long dur, long long guard) {
+  int j;
+  longlong2 g = make_longlong2(0, 0);
+  bool have = false;
+  if (c >= -1) {
+    const bool hn = c + 1 < v.n, hc = c >= 0;
+    const longlong2 nx = hn ? v.e[c + 1] : make_longlong2(0, 0);
+    const longlong2 cu = hc ? v.e[c] : make_longlong2(0, 0);
+    if (!hn || nx.x > x) {
+      j = c;
+      g = cu;
+      have = hc;
+    } else {
+      j = last_start_le_from(v, x, c);
+    }
+  } else {
+    j = last_start_le(v, x);
+  }
+  c = j;
+  if (j >= 0) {
+    if (!have) g = v.e[j];
+    if (x + dur <= gap_ue(g, guard)) return x;
+    if (dur == 0 && j >= 1) {
+      const longlong2 q = v.e[j - 1];
+      if ((q.y & (kGapFl - 1)) == x && gap_ue(q, guard) >= x) return x;
+    }
+  }
+  // next_start_from(v, j, dur, guard), with the previous gap carried
+  for (++j; j < v.n; ++j) {
+    const longlong2 e = v.e[j];
+    if (e.x + dur <= gap_ue(e, guard)) return e.x;
+    if (dur == 0 && j >= 1 && (g.y & (kGapFl - 1)) == e.x && gap_ue(g, guard) >= e.x) return e.x;
+    g = e;
+  }
+  return kInf64;
 }
 __device__ __forceinline__ long long next_start_from(const ListView& v, int j, long long dur,
                                                      long long guard) {
   for (++j; j < v.n; ++j) {
-    const long long st = v.lo[j];
+    const long long st = v.lo(j);
     if (st + dur <= usable_end(v, j, guard)) return st;
-    if (dur == 0 && j >= 1 && v.hi[j - 1] == st && usable_end(v, j - 1, guard) >= st) return st;
+    if (dur == 0 && j >= 1 && v.hi(j - 1) == st && usable_end(v, j - 1, guard) >= st) return st;
   }
   return kInf64;
 }
@@ -303,9 +351,7 @@ __device__ __forceinline__ long long next_start_from(const ListView& v, int j, l
 __device__ __forceinline__ ListView base_view(const PackArgs& a, const TlSlot& sl, int li) {
   ListView v;
   const long long go = sl.gap_off + (long long)li * (2 * sl.M + 1);
-  v.lo = a.glo + go;
-  v.hi = a.ghi + go;
-  v.fl = a.gflag + go;
+  v.e = a.gpk + go;
   v.n = a.gcnt[sl.lst_off + li];
   return v;
 }
@@ -321,7 +367,7 @@ __device__ __forceinline__ long long zero_run_shift(const ListView& v, long long
   long long i = 0;
   for (;;) {
     const long long x = x0 + i * step;
-    while (j + 1 < v.n && v.lo[j + 1] <= x) ++j;
+    while (j + 1 < v.n && v.lo(j + 1) <= x) ++j;
     if (!fits_at(v, j, x, 0, guard)) {
       const long long st = next_start_from(v, j, 0, guard);
       return st == kInf64 ? kInf64 : st - x;
@@ -362,11 +408,7 @@ __device__ bool ensure_private(const PackArgs& a, const TlSlot& sl, long long gb
   const long long noff = pool_base + bump;
   bump += ncap;
   ListView v = view_of(a, sl, gb, gi, li_shared);
-  for (int j = 0; j < n; ++j) {
-    a.pool_lo[noff + j] = v.lo[j];
-    a.pool_hi[noff + j] = v.hi[j];
-    a.pool_fl[noff + j] = v.fl[j];
-  }
+  for (int j = 0; j < n; ++j) a.pool[noff + j] = v.e[j];
   a.gpu_off[gb + gi] = noff;
   a.gpu_cnt[gb + gi] = n;
   a.gpu_cap[gb + gi] = ncap;
@@ -379,8 +421,8 @@ __device__ bool ensure_private(const PackArgs& a, const TlSlot& sl, long long gb
 __device__ __forceinline__ long long room_after(const ListView& v, long long a, long long guard) {
   long long best = -1;
   for (int j = v.n - 1; j >= 0; --j) {
-    if (v.hi[j] < a) break;  // gaps are sorted: every earlier gap ends before a
-    const long long ue = usable_end(v, j, guard), lo = max(v.lo[j], a);
+    if (v.hi(j) < a) break;  // gaps are sorted: every earlier gap ends before a
+    const long long ue = usable_end(v, j, guard), lo = max(v.lo(j), a);
     if (ue >= lo) best = max(best, ue - lo);
   }
   return best;
@@ -449,7 +491,7 @@ __device__ __forceinline__ long long group_search(const PackArgs& a, const TlSlo
   auto stage_lim = [&](const ListView& v, int k) {
     const long long dk = rg.dur(k);
     int j = v.n - 1;
-    while (j >= 0 && usable_end(v, j, a.guard_ns) - v.lo[j] < dk) --j;
+    while (j >= 0 && usable_end(v, j, a.guard_ns) - v.lo(j) < dk) --j;
     return j < 0 ? -kInf64 : usable_end(v, j, a.guard_ns) - dk - rg.off(k);
   };
   if (active) {
@@ -462,7 +504,7 @@ __device__ __forceinline__ long long group_search(const PackArgs& a, const TlSlo
       const ListView v = base_view(a, sl, li);
       long long ue = -kInf64;
       for (int j = v.n - 1; j >= 0 && ue == -kInf64; --j)
-        if (usable_end(v, j, a.guard_ns) >= v.lo[j]) ue = usable_end(v, j, a.guard_ns);
+        if (usable_end(v, j, a.guard_ns) >= v.lo(j)) ue = usable_end(v, j, a.guard_ns);
       lim = min(lim, ue == -kInf64 ? -kInf64 : ue - rg.off(sl.D - 1));
     }
   }
@@ -480,11 +522,8 @@ __device__ __forceinline__ long long group_search(const PackArgs& a, const TlSlo
         const int k = gl + p * gs;
         if (k < D && prop != kInf64) {
           const long long off = rg.off(k), dk = rg.dur(k);
-          const int j = last_start_le_from(vv[p], t + off, cur[p]);
-          if (!fits_at(vv[p], j, t + off, dk, a.guard_ns)) {
-            const long long st = next_start_from(vv[p], j, dk, a.guard_ns);
-            prop = st == kInf64 ? kInf64 : max(prop, st - off);
-          }
+          const long long st = stage_next(vv[p], cur[p], t + off, dk, a.guard_ns);
+          if (st != t + off) prop = st == kInf64 ? kInf64 : max(prop, st - off);
         }
       }
       for (int k = gl + kP * gs; k < D && prop != kInf64; k += gs) {
@@ -758,7 +797,7 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
             j = fitting_gap(v0, lo, hi - lo, a.guard_ns);
             // a zero-length interval at a gap end changes nothing (upper_bound
             // insertion behind the span that ends the gap)
-            need = j >= 0 && lo != v0.hi[j];
+            need = j >= 0 && lo != v0.hi(j);
             const long long off = a.gpu_off[gb + gi];
             n = v0.n;
             const int cap = off >= 0 ? a.gpu_cap[gb + gi] : 0;
@@ -777,49 +816,26 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
           if (ncap > 0) {  // private copy with room
             const long long noff = pool_base + bump + (incl - ncap);
             const ListView v = view_of(a, sl, gb, gi, li);
-            for (int x = 0; x < n; ++x) {
-              a.pool_lo[noff + x] = v.lo[x];
-              a.pool_hi[noff + x] = v.hi[x];
-              a.pool_fl[noff + x] = v.fl[x];
-            }
+            for (int x = 0; x < n; ++x) a.pool[noff + x] = v.e[x];
             a.gpu_off[gb + gi] = noff;
             a.gpu_cnt[gb + gi] = n;
             a.gpu_cap[gb + gi] = ncap;
           }
           bump += total;
           if (need) {
-            long long* L = a.pool_lo + a.gpu_off[gb + gi];
-            long long* Hh = a.pool_hi + a.gpu_off[gb + gi];
-            unsigned char* Fl = a.pool_fl + a.gpu_off[gb + gi];
-            const long long glo = L[j], ghi = Hh[j];
-            const unsigned char gfl = Fl[j];
+            longlong2* E = a.pool + a.gpu_off[gb + gi];
+            const longlong2 gj = E[j];
+            const long long glo = gj.x, ghi = gj.y & (kGapFl - 1), gfl = gj.y & kGapFl;
             const int add_l = lo > glo, add_r = ghi > hi;
             const int delta = add_l + add_r - 1;
             if (delta > 0) {
-              for (int x = n - 1; x > j; --x) {
-                L[x + 1] = L[x];
-                Hh[x + 1] = Hh[x];
-                Fl[x + 1] = Fl[x];
-              }
+              for (int x = n - 1; x > j; --x) E[x + 1] = E[x];
             } else if (delta < 0) {
-              for (int x = j + 1; x < n; ++x) {
-                L[x - 1] = L[x];
-                Hh[x - 1] = Hh[x];
-                Fl[x - 1] = Fl[x];
-              }
+              for (int x = j + 1; x < n; ++x) E[x - 1] = E[x];
             }
             int w = j;
-            if (add_l) {
-              L[w] = glo;
-              Hh[w] = lo;
-              Fl[w] = 0;  // the next span is this prefill
-              ++w;
-            }
-            if (add_r) {
-              L[w] = hi;
-              Hh[w] = ghi;
-              Fl[w] = gfl;
-            }
+            if (add_l) E[w++] = make_longlong2(glo, lo);  // the next span is this prefill
+            if (add_r) E[w] = make_longlong2(hi, ghi | gfl);
             a.gpu_cnt[gb + gi] = n + delta;
           }
           __syncwarp();
@@ -942,7 +958,10 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
             if (a.gpu_off[gb + gi] >= 0) {
               asum = 0;
               const long long o = a.gpu_off[gb + gi];
-              for (int x = 0; x < a.gpu_cnt[gb + gi]; ++x) asum += a.pool_hi[o + x] - a.pool_lo[o + x];
+              for (int x = 0; x < a.gpu_cnt[gb + gi]; ++x) {
+                const longlong2 g = a.pool[o + x];
+                asum += (g.y & (kGapFl - 1)) - g.x;
+              }
             }
             ua = __dadd_rn(ua, __ddiv_rn((double)(H - asum), (double)H));
           }
@@ -1051,7 +1070,8 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
   long long* fe = (long long*)c.dev_buf(c.b_tl_spans, 16 * (size_t)std::max(1LL, tl));
   long long* ps = fe + std::max(1LL, tl);
   gpb_row* tl_rows = (gpb_row*)c.dev_buf(c.b_tl_rows, sizeof(gpb_row) * (size_t)c.n_rows);
-  long long* glo = (long long*)c.dev_buf(c.b_gaps, 17 * (size_t)std::max(1LL, gp));
+  longlong2* gpk = (longlong2*)c.dev_buf(c.b_gaps, 33 * (size_t)std::max(1LL, gp));
+  long long* glo = (long long*)(gpk + std::max(1LL, gp));
   long long* ghi = glo + std::max(1LL, gp);
   unsigned char* gfl = (unsigned char*)(ghi + std::max(1LL, gp));
   int* gcnt = (int*)c.dev_buf(c.b_ngaps, 24 * (size_t)std::max(1LL, ls) + 8 * (size_t)n + 64);
@@ -1142,7 +1162,7 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
   long long max_lists = 1;
   for (const TlSlot& s : slots) max_lists = std::max(max_lists, (long long)s.Ce * s.S);
   gap_kernel<<<dim3((unsigned)((max_lists + 127) / 128), (unsigned)n), 128, 0, st>>>(
-      dslots, n, fe, ps, ar_dev, ar_start, glo, ghi, gfl, gcnt, gsum, ghas, hz);
+      dslots, n, fe, ps, ar_dev, ar_start, glo, ghi, gfl, gpk, gcnt, gsum, ghas, hz);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return c.cuda_fail(e, "gap kernel");
   int32_t flag = 0;
@@ -1155,6 +1175,7 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
   c.tl_glo = glo;
   c.tl_ghi = ghi;
   c.tl_gfl = gfl;
+  c.tl_gpk = gpk;
   c.tl_gcnt = gcnt;
   c.tl_gsum = gsum;
   c.tl_ghas = ghas;
@@ -1329,8 +1350,8 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
                                (long long)slots[i].D * std::min<long long>(n_req, 2048)));
   }
   for (int attempt = 0; attempt < 8; ++attempt) {
-    long long* pool_lo = (long long*)c.dev_buf(c.b_tl_scratch, 17 * (size_t)pool * std::max(1, n_rows_sel));
-    if (!pool_lo) return c.cuda_fail(cudaErrorMemoryAllocation, "pack pool");
+    longlong2* pool_e = (longlong2*)c.dev_buf(c.b_tl_scratch, 16 * (size_t)pool * std::max(1, n_rows_sel));
+    if (!pool_e) return c.cuda_fail(cudaErrorMemoryAllocation, "pack pool");
     PackArgs a;
     std::memset(&a, 0, sizeof a);
     a.slots = (const TlSlot*)c.tl_slots_dev;
@@ -1338,9 +1359,7 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
     a.scens = (const DevScen*)c.b_scens.ptr;
     a.topos = (const DevTopo*)c.b_topos.ptr;
     a.row_scen = (const int32_t*)c.b_row_scen.ptr;
-    a.glo = c.tl_glo;
-    a.ghi = c.tl_ghi;
-    a.gflag = c.tl_gfl;
+    a.gpk = c.tl_gpk;
     a.gcnt = c.tl_gcnt;
     a.gsum = c.tl_gsum;
     a.hz = c.tl_hz;
@@ -1355,9 +1374,7 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
     a.bpe = pm->bytes_per_element;
     a.inf_hidden = pm->inference_hidden;
     a.guard_ns = host_ms_to_ns(pm->guard_ms);
-    a.pool_lo = pool_lo;
-    a.pool_hi = pool_lo + pool * n_rows_sel;
-    a.pool_fl = (unsigned char*)(a.pool_hi + pool * n_rows_sel);
+    a.pool = pool_e;
     a.pool_per_slot = pool;
     a.gpu_off = gpu_off;
     a.gpu_cnt = gpu_cnt;

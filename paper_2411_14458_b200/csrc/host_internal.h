@@ -86,6 +86,7 @@ struct Ctx {
   // last build_timelines() outputs (device pointers into the buffers above)
   long long *tl_glo = nullptr, *tl_ghi = nullptr, *tl_gsum = nullptr, *tl_hz = nullptr;
   unsigned char* tl_gfl = nullptr;
+  longlong2* tl_gpk = nullptr;  // packed copy of the gap lists (pack kernel)
   int *tl_gcnt = nullptr, *tl_ghas = nullptr;
   void* tl_slots_dev = nullptr;
   bool timing_valid = false;

@@ -157,11 +157,28 @@ __device__ __forceinline__ void warp_merge(long long* A, int na, const long long
   __syncwarp();
 }
 
+// Cursor into a static list: index i and the entry there (kEndCur past the
+// end), so the common "no advance" check needs no load.
+constexpr long long kEndCur = 1LL << 60;
+struct LinkCur {
+  int i;
+  long long v;
+  __device__ __forceinline__ void reset(const long long* mg, int n) {
+    i = 0;
+    v = n > 0 ? mg[0] : kEndCur;
+  }
+  __device__ __forceinline__ void set(const long long* mg, int n, int k) {
+    i = k;
+    v = k < n ? mg[k] : kEndCur;
+  }
+};
+
 // Advance the cursor to the first static entry ending after x (gallop from
 // the cursor, then bisect).
-__device__ __forceinline__ void link_advance(const long long* mg, int n, int& cur, long long len,
+__device__ __forceinline__ void link_advance(const long long* mg, int n, LinkCur& c, long long len,
                                              long long x) {
-  if (cur >= n || mg[cur] + len > x) return;
+  if (c.v + len > x) return;
+  const int cur = c.i;
   int lo = cur + 1, step = 1;
   while (lo + step - 1 < n && mg[lo + step - 1] + len <= x) {
     lo += step;
@@ -172,7 +189,7 @@ __device__ __forceinline__ void link_advance(const long long* mg, int n, int& cu
     const int mid = (lo + hi) >> 1;
     if (mg[mid] + len <= x) lo = mid + 1; else hi = mid;
   }
-  cur = lo;
+  c.set(mg, n, lo);
 }
 
 // Run jumps of a static list whose intervals all have length len:
@@ -195,26 +212,26 @@ __device__ __forceinline__ void warp_jumps(const long long* mg, int n, long long
 }
 
 // [x, x+len) overlaps a static entry (cursor `cur`, advanced) or the own tail
-__device__ __forceinline__ bool link_conflict(const long long* mg, int n, int& cur,
+__device__ __forceinline__ bool link_conflict(const long long* mg, int n, LinkCur& c,
                                               long long own_last, long long len, long long x) {
   if (len <= 0) return false;
-  link_advance(mg, n, cur, len, x);
-  if (cur < n && mg[cur] < x + len) return true;
+  link_advance(mg, n, c, len, x);
+  if (c.v < x + len) return true;
   return own_last + len > x;
 }
 
 // earliest_fit over the static list and the own tail; a run of back-to-back
 // static entries is crossed in one step through the jump table
-__device__ __forceinline__ long long link_fit(const long long* mg, const int* jmp, int n, int& cur,
+__device__ __forceinline__ long long link_fit(const long long* mg, const int* jmp, int n, LinkCur& c,
                                               long long own_last, long long len, long long x) {
   if (len <= 0) return x;
   long long t = x;
   for (;;) {
-    link_advance(mg, n, cur, len, t);
-    if (cur < n && mg[cur] < t + len) {
-      cur = jmp[cur];
-      t = mg[cur] + len;
-      ++cur;
+    link_advance(mg, n, c, len, t);
+    if (c.v < t + len) {
+      const int k = jmp[c.i];
+      t = mg[k] + len;
+      c.set(mg, n, k + 1);
       continue;
     }
     if (own_last + len > t) {
@@ -250,19 +267,20 @@ __device__ __forceinline__ long long link_fit(const long long* mg, const int* jm
 // are resolved top-down (the topmost conflicting WAN stage has a final
 // input), rescanning after each, so a round costs 1 + (#shifted WAN stages)
 // scans instead of one sequential step per pair.
-constexpr long long kNegMP = -(1LL << 62);
+// -inf of the max-plus maps. Real times and their sums along a row stay
+// below 2^50 ns (13 days) and a composed map sums at most 256 terms (one
+// per stage), so plain adds never overflow (|sum| < 2^62) and a map that
+// includes a -inf term stays negative, below every real time (no clamping).
+constexpr long long kNegMP = -(1LL << 53);
 
-__device__ __forceinline__ long long mp_add(long long x, long long y) {
-  const long long r = x + y;  // |x|,|y| <= 2^62: no overflow
-  return r < kNegMP ? kNegMP : r;
-}
+__device__ __forceinline__ long long mp_add(long long x, long long y) { return x + y; }
 
 template <int B, bool TIMELINE>
 __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L, AtlasMem& X,
                                               long long (&gfr)[B], int (&drr)[B],
                                               const int (&wbi)[B], const long long (&serb)[B],
                                               const long long (&latb)[B],
-                                              long long (&ownb)[B], int (&mcur)[B],
+                                              long long (&ownb)[B], LinkCur (&mcur)[B],
                                               const int (&mn)[B], long long& n_pairs,
                                               long long& n_scans, long long& n_rounds,
                                               long long* cph) {
@@ -350,8 +368,7 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
       }
       // inclusive suffix scan over the nl stage-owning lanes (higher lanes =
       // deeper stages first)
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {  // fixed trip count: no divergent shuffles
+      for (int o = 1; o < nl; o <<= 1) {  // warp-uniform trip count
         const long long oa = shfl_down64(ta, o), ob = shfl_down64(tb, o);
         if (lane + o < nl) {
           tb = imax(mp_add(ob, ta), tb);
@@ -436,7 +453,9 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
 //  * a stage without a WAN gradient link has no shared resource: pipeline
 //    p's pairs follow e[m] = max(r[m], e[m-1]) + dur, i.e.
 //    e[m] = (m+1)*dur + max(gf0 - m0*dur, max_{m0<=j<=m} (r[j] - j*dur)),
-//    one segmented prefix-max over the stage's (pipeline, microbatch) pairs;
+//    one segmented prefix-max over the stage's (pipeline, microbatch) pairs
+//    (drain_stage_scan); a deep run of such stages with few pairs is one
+//    2-D max-plus wavefront instead (drain_run_wavefront);
 //  * a stage with a WAN gradient link runs the greedy over its C pipelines
 //    (lane = pipeline, warp argmin, lowest pipeline on ties). Its link holds
 //    the forward phase's forced drains (a static merged list) plus this
@@ -450,11 +469,11 @@ __device__ void drain_stage_scan(const Geom& g, AtlasMem& X, int s) {
   const int lane = threadIdx.x & 31;
   const int S = g.S, M = g.M, C = g.C;
   const long long dur = g.dur;
-  const long long n = (long long)C * M;
+  const int n = C * M;
   long long carry = kNegMP;
-  for (long long base = 0; base < n; base += 32 * K) {
-    const long long rem = n - base < 32 * K ? n - base : 32 * K;
-    const int kk = (int)((rem + 31) / 32);
+  for (int base = 0; base < n; base += 32 * K) {
+    const int rem = n - base < 32 * K ? n - base : 32 * K;
+    const int kk = (rem + 31) / 32;
     long long u[K];
     bool rs[K], act[K];
     int rs_first = K;
@@ -463,9 +482,9 @@ __device__ void drain_stage_scan(const Geom& g, AtlasMem& X, int s) {
     for (int i = 0; i < K; ++i) {
       u[i] = kNegMP;
       rs[i] = act[i] = false;
-      const long long idx = base + (long long)lane * kk + i;
+      const int idx = base + lane * kk + i;
       if (i < kk && idx < base + rem) {
-        const int p = (int)(idx / M), m = (int)(idx - (long long)p * M);
+        const int p = idx / M, m = idx - p * M;
         const int m0 = X.nm[p * S + s];
         if (m >= m0) {
           act[i] = true;
@@ -511,8 +530,8 @@ __device__ void drain_stage_scan(const Geom& g, AtlasMem& X, int s) {
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       if (!act[i]) continue;
-      const long long idx = base + (long long)lane * kk + i;
-      const int p = (int)(idx / M), m = (int)(idx - (long long)p * M);
+      const int idx = base + lane * kk + i;
+      const int p = idx / M, m = idx - p * M;
       const long long uu = i >= rs_first ? u[i] : imax(pre, u[i]);
       const long long e = (long long)(m + 1) * dur + uu;
       if (s > 0) X.garr[((size_t)p * S + s - 1) * M + m] = e;
@@ -524,6 +543,74 @@ __device__ void drain_stage_scan(const Geom& g, AtlasMem& X, int s) {
   }
   __syncwarp();
   for (int p = lane; p < C; p += 32) X.nm[p * S + s] = M;
+  __syncwarp();
+}
+
+// A run of consecutive stages s_top..s_bot none of which has a WAN gradient
+// link: every pair follows e[p][s][m] = max(in[p][s][m], e[p][s][m-1]) +
+// dur, with in = the output of stage s+1 for the same pair (or the forward
+// end at S-1), and the chain of each (p, s) starting from its gpu_free at
+// its first pair not drained in the forward phase. That is a 2-D max-plus
+// grid evaluated as one wavefront: lane l owns stages s_top - l*Bw - j
+// (j < Bw) and handles pair k = (p, m) at step k + l, taking the output of
+// the lane above from the previous step by shuffle; a pair drained in the
+// forward phase passes nothing and its consumer reads the stored gradient.
+// Runs longer than 32*B stages are split by the caller.
+template <int B, bool TIMELINE>
+__device__ void drain_run_wavefront(const Geom& g, AtlasMem& X, int s_top, int s_bot) {
+  const int lane = threadIdx.x & 31;
+  const int S = g.S, M = g.M, C = g.C;
+  const long long dur = g.dur;
+  const int R = s_top - s_bot + 1;
+  const int Bw = (R + 31) / 32;  // <= B
+  const int nl = (R + Bw - 1) / Bw;
+  const int n = C * M;
+  int sj[B], nmj[B];
+  long long pe[B];
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    sj[j] = j < Bw && lane < nl ? s_top - lane * Bw - j : -1;
+    if (sj[j] < s_bot) sj[j] = -1;
+    nmj[j] = 0;
+    pe[j] = 0;
+  }
+  long long xo = 0;  // this lane's output of the previous step
+  bool fo = false;   // ... and whether its bottom stage computed it
+  for (int t = 0; t < n + nl - 1; ++t) {
+    long long x = shfl_up64(xo, 1);
+    bool f = __shfl_up_sync(kFull, (int)fo, 1) != 0;
+    if (lane == 0) f = false;
+    const int k = t - lane;
+    if (lane < nl && k >= 0 && k < n) {
+      const int p = k / M, m = k - p * M;
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const int s = sj[j];
+        if (s < 0) continue;
+        if (m == 0) {
+          nmj[j] = X.nm[p * S + s];
+          pe[j] = X.gf[p * S + s];
+        }
+        if (m < nmj[j]) {  // drained in the forward phase
+          f = false;
+          continue;
+        }
+        const long long r = f ? x : (s == S - 1 ? X.fdl[p * M + m]
+                                                : X.garr[((size_t)p * S + s) * M + m]);
+        const long long e = imax(r, pe[j]) + dur;
+        pe[j] = e;
+        if (s == s_bot && s > 0) X.garr[((size_t)p * S + s - 1) * M + m] = e;
+        if (TIMELINE) X.ps[((size_t)p * S + s) * M + m] = e - dur;
+        if (m == M - 1) X.gf[p * S + s] = e;
+        x = e;
+        f = true;
+      }
+    }
+    xo = x;
+    fo = f;
+  }
+  __syncwarp();
+  for (int i = lane; i < C * R; i += 32) X.nm[(i / R) * S + s_bot + i % R] = M;
   __syncwarp();
 }
 
@@ -539,7 +626,8 @@ __device__ void drain_stage_greedy(const Geom& g, AtlasMem& X, int s, int w) {
   const int nmg = X.mcnt[8 + w];
   int mq = q < C ? X.nm[q * S + s] : M;
   long long gfq = q < C ? X.gf[q * S + s] : 0;
-  int cur = 0;
+  LinkCur cur;
+  cur.reset(mg, nmg);
   long long last_a = kNegMP;  // start of this stage's last committed transfer
   auto fresh = [&]() -> long long {
     const long long r = s == S - 1 ? X.fdl[q * M + mq] : X.garr[((size_t)q * S + s) * M + mq];
@@ -580,6 +668,8 @@ __device__ void drain_stage_greedy(const Geom& g, AtlasMem& X, int s, int w) {
   }
   __syncwarp();
 }
+
+constexpr int kWaveRatio = 8;
 
 template <int B, bool TIMELINE>
 __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& err,
@@ -650,7 +740,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
   int drr[B];
   if (lane < 8) X.mcnt[lane] = X.mcnt[8 + lane] = 0;
   __syncwarp();
-  int curf = 0;  // lane w: cursor of the static forward list of link w
+  LinkCur curf;  // lane w: cursor of the static forward list of link w
   for (int p = 0; p < C; ++p) {
 #pragma unroll
     for (int j = 0; j < B; ++j) {
@@ -675,15 +765,17 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
         __syncwarp();
       }
     }
-    curf = 0;
     __syncwarp();
     long long ownb[B];
-    int mcur[B], mn[B];
+    LinkCur mcur[B];
+    int mn[B];
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       ownb[j] = kNegMP;
-      mcur[j] = 0;
       mn[j] = wbi[j] >= 0 ? X.mcnt[8 + wbi[j]] : 0;
+      mcur[j].i = 0;
+      mcur[j].v = kEndCur;
+      if (wbi[j] >= 0) mcur[j].reset(X.mb + (size_t)wbi[j] * C * M, mn[j]);
     }
     // lane w < nw: link w's constants for this pipeline (chain checks)
     long long aw_l = 0, lenw_l = 0, ownw_l = kNegMP;
@@ -695,6 +787,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
       mgw_l = X.mf + (size_t)lane * C * M;
       jgw_l = X.jf + (size_t)lane * C * M;
       nmw_l = X.mcnt[lane];
+      curf.reset(mgw_l, nmw_l);
     }
     for (int m = 0; m < M; ++m) {
       // memory-cap admission (:366-381) + forced drains (:321-346)
@@ -813,13 +906,26 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     if (lane == 0) X.mcnt[8 + w] = nbk + add_b;
     __syncwarp();
   }
-  for (int s = S - 1; s >= 0; --s) {
+  for (int s = S - 1; s >= 0;) {
     const int w = X.wbs[s];
-    if (w < 0) {
-      drain_stage_scan<TIMELINE>(g, X, s);
-    } else {
+    if (w >= 0) {
       drain_stage_greedy<TIMELINE>(g, X, s, w);
+      --s;
+      continue;
     }
+    int sb = s;  // the run of stages without a WAN gradient link below s
+    while (sb > 0 && X.wbs[sb - 1] < 0) --sb;
+    // per-stage scans cost ~R * ceil(CM / 256) scan steps, the wavefront
+    // CM + R/B shuffle steps (kWaveRatio: measured cost ratio of the two)
+    const int R = s - sb + 1, CM = C * g.M;
+    if ((long long)(CM + (R + B - 1) / B) > (long long)kWaveRatio * R * ((CM + 255) / 256)) {
+      for (; s >= sb; --s) drain_stage_scan<TIMELINE>(g, X, s);
+      continue;
+    }
+    constexpr int BW = B < 4 ? B : 4;  // stages per lane (register arrays)
+    for (int st = s; st >= sb; st -= 32 * BW)
+      drain_run_wavefront<BW, TIMELINE>(g, X, st, max(sb, st - 32 * BW + 1));
+    s = sb - 1;
   }
   if (phase && lane == 0) {
     ph_drain = clock64() - ph_t;
