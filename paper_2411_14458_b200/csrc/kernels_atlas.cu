@@ -576,10 +576,22 @@ __device__ void drain_run_wavefront(const Geom& g, AtlasMem& X, int s_top, int s
   }
   long long xo = 0;  // this lane's output of the previous step
   bool fo = false;   // ... and whether its bottom stage computed it
+  long long top = 0;  // inputs of the run's top stage, items [t & ~31, +32), lane i = item +i
   for (int t = 0; t < n + nl - 1; ++t) {
+    if ((t & 31) == 0 && t < n) {  // coalesced prefetch of the next 32 top inputs
+      const int k = t + lane;
+      if (k < n) {
+        const int p = k / M, m = k - p * M;
+        top = s_top == S - 1 ? X.fdl[p * M + m] : X.garr[((size_t)p * S + s_top) * M + m];
+      }
+    }
     long long x = shfl_up64(xo, 1);
     bool f = __shfl_up_sync(kFull, (int)fo, 1) != 0;
-    if (lane == 0) f = false;
+    const long long tv = shfl_idx64(top, t & 31);
+    if (lane == 0) {
+      x = tv;
+      f = true;  // (a top stage always consumes the stored input)
+    }
     const int k = t - lane;
     if (lane < nl && k >= 0 && k < n) {
       const int p = k / M, m = k - p * M;
@@ -629,16 +641,24 @@ __device__ void drain_stage_greedy(const Geom& g, AtlasMem& X, int s, int w) {
   LinkCur cur;
   cur.reset(mg, nmg);
   long long last_a = kNegMP;  // start of this stage's last committed transfer
+  // inputs of this stage are final (stage s+1 is drained): the next pair's
+  // input is loaded one commit ahead
+  auto input = [&](int m) -> long long {
+    return s == S - 1 ? X.fdl[q * M + m] : X.garr[((size_t)q * S + s) * M + m];
+  };
+  long long rnext = q < C && mq < M ? input(mq) : 0;
   auto fresh = [&]() -> long long {
-    const long long r = s == S - 1 ? X.fdl[q * M + mq] : X.garr[((size_t)q * S + s) * M + mq];
+    const long long r = rnext;
+    if (mq + 1 < M) rnext = input(mq + 1);
     return link_fit(mg, jg, nmg, cur, last_a, len, imax(r, gfq) + dur) - dur;
   };
   long long cand = mq < M ? fresh() : kInf64;
+  int P2 = 1;  // argmin over the lowest power-of-two group holding the C lanes
+  while (P2 < C) P2 <<= 1;
   for (;;) {
     long long b = cand;
     int bq = q;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = P2 >> 1; o > 0; o >>= 1) {
       const long long ob = __shfl_xor_sync(kFull, b, o);
       const int oq = __shfl_xor_sync(kFull, bq, o);
       if (ob < b || (ob == b && oq < bq)) {
@@ -646,6 +666,8 @@ __device__ void drain_stage_greedy(const Geom& g, AtlasMem& X, int s, int w) {
         bq = oq;
       }
     }
+    b = shfl_idx64(b, 0);
+    bq = __shfl_sync(kFull, bq, 0);
     if (b == kInf64) break;
     if (q == bq) {  // atlas_commit_pair (:298-317) + reserve
       const long long e = b + dur;
@@ -906,11 +928,14 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     if (lane == 0) X.mcnt[8 + w] = nbk + add_b;
     __syncwarp();
   }
+  long long dph[4] = {0, 0, 0, 0};  // drain: greedy / scan / wavefront cycles, wave steps
   for (int s = S - 1; s >= 0;) {
+    const long long td = phase ? clock64() : 0;
     const int w = X.wbs[s];
     if (w >= 0) {
       drain_stage_greedy<TIMELINE>(g, X, s, w);
       --s;
+      if (phase) dph[0] += clock64() - td;
       continue;
     }
     int sb = s;  // the run of stages without a WAN gradient link below s
@@ -920,12 +945,17 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     const int R = s - sb + 1, CM = C * g.M;
     if ((long long)(CM + (R + B - 1) / B) > (long long)kWaveRatio * R * ((CM + 255) / 256)) {
       for (; s >= sb; --s) drain_stage_scan<TIMELINE>(g, X, s);
+      if (phase) dph[1] += clock64() - td;
       continue;
     }
     constexpr int BW = B < 4 ? B : 4;  // stages per lane (register arrays)
-    for (int st = s; st >= sb; st -= 32 * BW)
-      drain_run_wavefront<BW, TIMELINE>(g, X, st, max(sb, st - 32 * BW + 1));
+    for (int st = s; st >= sb; st -= 32 * BW) {
+      const int bot = max(sb, st - 32 * BW + 1), rr = st - bot + 1;
+      drain_run_wavefront<BW, TIMELINE>(g, X, st, bot);
+      dph[3] += CM + (rr + BW - 1) / BW;
+    }
     s = sb - 1;
+    if (phase) dph[2] += clock64() - td;
   }
   if (phase && lane == 0) {
     ph_drain = clock64() - ph_t;
@@ -938,6 +968,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     phase[6] = n_adm;
     phase[7] = n_rounds;
     for (int k = 0; k < 4; ++k) phase[8 + k] = cph[k];
+    for (int k = 0; k < 4; ++k) phase[12 + k] = dph[k];
   }
   // -------------------------------------------- right-pack (timeline)
   if (TIMELINE) {

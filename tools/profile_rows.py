@@ -37,8 +37,9 @@ for r, c, ph in zip(rows[:n], cyc, phase):
 tot = sum(v[1] for v in agg.values())
 print(json.dumps({"evaluate_ms": t.evaluate_ms, "policy_ms": list(t.policy_ms)}))
 print("policy S C M feas | rows  sum_Mcyc  share  max_kcyc")
-for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:25]:
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:int(sys.argv[2]) if len(sys.argv) > 2 else 25]:
     ph = [round(x / max(1, v[1]) * 100) for x in v[3][:4]] + [round(x / v[0]) for x in v[3][4:8]] \
-        + [round(x / max(1, v[1]) * 100) for x in v[3][8:12]]
+        + [round(x / max(1, v[1]) * 100) for x in v[3][8:12]] \
+        + [round(x / max(1, v[1]) * 100) for x in v[3][12:15]] + [round(v[3][15] / v[0])]
     print(*k, "|", v[0], round(v[1] / 1e6, 2), f"{100 * v[1] / tot:.1f}%", round(v[2] / 1e3, 1),
-          "phases% casc/chain/fit/drain + per-row scans/pairs/adm/rounds + casc% setup/loads/scan/commit", ph)
+          "phases% casc/chain/fit/drain + per-row scans/pairs/adm/rounds + casc% setup/loads/scan/commit + drain% greedy/scan/wave + wave steps", ph)
