@@ -555,121 +555,6 @@ __device__ __forceinline__ long long group_search(const PackArgs& a, const TlSlo
   return t;
 }
 
-// Phase-1 search of one request per lane (see pack_kernel): the lane walks
-// the pipelines in order (caps and memo filters) and runs group_search's
-// leapfrog with a group of one, but as a flat per-lane state machine — a
-// lane that finishes a search starts its next one in the next warp step
-// instead of waiting for the slowest lane's search. Returns the first
-// pipeline with a feasible start (pipe1, t1) or pipe1 = -1; failm collects
-// the failed pipelines < 64.
-template <int kP>
-__device__ __forceinline__ void lane_search_all(const PackArgs& a, const TlSlot& sl, long long gb,
-                                                bool act, long long arrival, const ReqGeom& rg,
-                                                bool zrun, const long long* capA,
-                                                const long long* capB, const unsigned* memo,
-                                                int tok, int n_pipes, int& pipe1, long long& t1,
-                                                unsigned long long& failm, long long& iters,
-                                                long long& n_search, long long& n_fail) {
-  const int S = sl.S, C = sl.C;
-  const int D = zrun ? rg.extra : sl.D;  // stages searched one by one
-  int next = 0, pipe = 0, stage = 0, li = 0, pi = -1;
-  bool done = !act, busy = false;
-  long long t = 0, lim = 0;
-  ListView vv[kP];
-  int cur[kP];
-  auto stage_lim = [&](const ListView& v, int k) {
-    const long long dk = rg.dur(k);
-    int j = v.n - 1;
-    while (j >= 0 && usable_end(v, j, a.guard_ns) - v.lo(j) < dk) --j;
-    return j < 0 ? -kInf64 : usable_end(v, j, a.guard_ns) - dk - rg.off(k);
-  };
-  pipe1 = -1;
-  t1 = kInf64;
-  while (__any_sync(kFull, !done)) {
-    ++iters;
-    if (done) continue;
-    if (!busy) {  // start the search of the next candidate pipeline
-      pi = -1;
-      for (; next < n_pipes; ++next) {
-        if (rg.d0 <= capB[next] && (rg.extra == 0 || rg.d1 <= capA[next]) &&
-            !((memo[(size_t)next * a.memo_words + (tok >> 5)] >> (tok & 31)) & 1u)) {
-          pi = next++;
-          break;
-        }
-      }
-      if (pi < 0) {
-        done = true;
-        continue;
-      }
-      ++n_search;
-      pipe = pi / S;
-      stage = pi % S;
-      li = (sl.Ce > 1 ? pipe : 0) * S + stage;
-      t = arrival;
-      lim = kInf64;
-#pragma unroll
-      for (int p = 0; p < kP; ++p) {
-        cur[p] = -2;
-        if (p < D) {
-          vv[p] = view_of(a, sl, gb, gpu_index(p, pipe, stage, C, S), li);
-          lim = min(lim, stage_lim(vv[p], p));
-        }
-      }
-      for (int k = kP; k < D; ++k)
-        lim = min(lim, stage_lim(view_of(a, sl, gb, gpu_index(k, pipe, stage, C, S), li), k));
-      if (zrun) {
-        const ListView v = base_view(a, sl, li);
-        long long ue = -kInf64;
-        for (int j = v.n - 1; j >= 0 && ue == -kInf64; --j)
-          if (usable_end(v, j, a.guard_ns) >= v.lo(j)) ue = usable_end(v, j, a.guard_ns);
-        lim = min(lim, ue == -kInf64 ? -kInf64 : ue - rg.off(sl.D - 1));
-      }
-      if (t > lim) {
-        ++n_fail;
-        if (pi < 64) failm |= 1ull << pi;
-      } else {
-        busy = true;
-      }
-      continue;
-    }
-    // one leapfrog step (group_search with a group of one lane)
-    long long prop = t;
-#pragma unroll
-    for (int p = 0; p < kP; ++p) {
-      if (p < D && prop != kInf64) {
-        const long long off = rg.off(p), dk = rg.dur(p);
-        const long long st = stage_next(vv[p], cur[p], t + off, dk, a.guard_ns);
-        if (st != t + off) prop = st == kInf64 ? kInf64 : max(prop, st - off);
-      }
-    }
-    for (int k = kP; k < D && prop != kInf64; ++k) {
-      const ListView v = view_of(a, sl, gb, gpu_index(k, pipe, stage, C, S), li);
-      const long long off = rg.off(k), dk = rg.dur(k);
-      if (fitting_gap(v, t + off, dk, a.guard_ns) < 0) {
-        const long long st = next_start(v, t + off, dk, a.guard_ns);
-        prop = st == kInf64 ? kInf64 : max(prop, st - off);
-      }
-    }
-    if (zrun && prop != kInf64) {  // the zero-length run
-      const long long sh = zero_run_shift(base_view(a, sl, li), t + rg.off(D), rg.ovh, sl.D - D,
-                                          a.guard_ns);
-      prop = sh == kInf64 ? kInf64 : max(prop, t + sh);
-    }
-    if (prop == kInf64 || prop > lim) {
-      busy = false;
-      ++n_fail;
-      if (pi < 64) failm |= 1ull << pi;
-    } else if (prop == t) {  // every stage fits at t
-      busy = false;
-      done = true;
-      pipe1 = pi;
-      t1 = t;
-    } else {
-      t = prop;
-    }
-  }
-}
-
 // Caps of pipeline pi at reference time `a_ref`, group-parallel over its
 // stages (see pipeline_caps); every lane of the group gets the result.
 __device__ __forceinline__ void group_caps(const PackArgs& a, const TlSlot& sl, long long gb,
@@ -795,13 +680,36 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
     // committed to that same pipeline (phase 2 re-searches those).
     const bool act = (todo0 >> lane) & 1u;
     const int tok_l = q.tokens - 1;
+    int pi_l = act ? 0 : n_pipes;
     int pipe1 = -1;
     long long t1 = kInf64;
     unsigned long long failm = 0;  // pipelines < 64 that failed this lane's search
     {
       const long long tc = clock64();
-      lane_search_all<8>(a, sl, gb, act, arrival, rg, zrun, capA, capB, memo, tok_l, n_pipes,
-                         pipe1, t1, failm, st_iter, st_search, st_fail);
+      for (;;) {
+        int cand = -1;
+        for (; pi_l < n_pipes; ++pi_l) {
+          if (rg.d0 <= capB[pi_l] && (extra == 0 || rg.d1 <= capA[pi_l]) &&
+              !((memo[(size_t)pi_l * a.memo_words + (tok_l >> 5)] >> (tok_l & 31)) & 1u)) {
+            cand = pi_l;
+            break;
+          }
+        }
+        if (!__any_sync(kFull, cand >= 0)) break;
+        st_search += cand >= 0;
+        const long long t = group_search<8>(a, sl, gb, cand, arrival, rg, 1, st_iter, zrun);
+        if (cand >= 0) {
+          if (t != kInf64) {
+            pipe1 = cand;
+            t1 = t;
+            pi_l = n_pipes;
+          } else {
+            ++st_fail;
+            if (cand < 64) failm |= 1ull << cand;
+            ++pi_l;
+          }
+        }
+      }
       st_cyc_search += clock64() - tc;
     }
     for (int i = lane; i < n_pipes; i += 32) cflag[i] = 0;

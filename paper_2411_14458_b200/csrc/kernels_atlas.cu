@@ -281,7 +281,8 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
                                               const int (&wbi)[B], const long long (&serb)[B],
                                               const long long (&latb)[B],
                                               long long (&ownb)[B], LinkCur (&mcur)[B],
-                                              const int (&mn)[B], long long& n_pairs,
+                                              const int (&mn)[B], const long long (&wsuf)[B],
+                                              long long& n_pairs,
                                               long long& n_scans, long long& n_rounds,
                                               long long* cph) {
   // ownb[j]: start of pipeline p's last reservation on stage j's gradient
@@ -346,50 +347,64 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
       cph[1] += t1 - ct;
       ct = t1;
     }
-    for (;;) {
-      ++n_scans;
-      // lane map: stages lane*B+B-1 (applied first) down to lane*B
-      long long ta = 0, tb = kNegMP;
+    // The round as one suffix max of one value per stage. A stage's pair
+    // starts at lo_s = max(in_s, gf_s); in_s is the output of the stage above
+    // (linked) or a stored gradient. With c_s = dur + dl_s + wl_s (dl: the
+    // exact-fit shift) and K_s = sum_{i >= s} c_i,
+    //   lo_s = K_s + max_{j in seg(s)} (base_j - K_j + c_j) - c_s,
+    // seg(s) = s and the linked stages above it up to the first "head" (a
+    // stage that is not linked, or idle this round: its output is -inf),
+    // base_j = gf_j, max(in_j, gf_j) at a head. The segments are separated
+    // by adding kSegBig * (#heads at or above j): every value above a
+    // segment is smaller by at least kSegBig (|base - K + c| < 2^51).
+    constexpr long long kSegBig = 1LL << 53;
+    long long hb[B];  // kSegBig * heads at or above the stage
+    {
+      int hc[B], loc = 0;
 #pragma unroll
       for (int j = B - 1; j >= 0; --j) {
-        long long fa = kNegMP, fb = kNegMP;
-        if (r < cnt[j]) {
-          const long long c = dur + dl[j] + wl[j];
-          if (link[j]) {
-            fa = c;
-            fb = gfr[j] + c;
-          } else {
-            fb = imax(xin[j], gfr[j]) + c;
-          }
-        }
-        // (F o T)(x) = max(x + ta + fa, max(tb + fa, fb))
-        ta = mp_add(ta, fa);
-        tb = imax(mp_add(tb, fa), fb);
+        const int s = lane * B + j;
+        if (s < S && (r >= cnt[j] || !link[j])) ++loc;
+        hc[j] = loc;
       }
-      // inclusive suffix scan over the nl stage-owning lanes (higher lanes =
-      // deeper stages first)
-      for (int o = 1; o < nl; o <<= 1) {  // warp-uniform trip count
-        const long long oa = shfl_down64(ta, o), ob = shfl_down64(tb, o);
-        if (lane + o < nl) {
-          tb = imax(mp_add(ob, ta), tb);
-          ta = mp_add(oa, ta);
-        }
+      int incl = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_down_sync(kFull, incl, o);
+        if (lane + o < 32) incl += v;
       }
-      long long v = shfl_down64(tb, 1);  // everything above this lane, at -inf
-      if (lane + 1 >= nl) v = kNegMP;
+#pragma unroll
+      for (int j = 0; j < B; ++j) hb[j] = kSegBig * (hc[j] + incl - loc);
+    }
+    long long DLs[B];  // sum of the shifts at stages >= s
+#pragma unroll
+    for (int j = 0; j < B; ++j) DLs[j] = 0;
+    for (;;) {
+      ++n_scans;
+      long long um[B], run = kNegMP;
+#pragma unroll
+      for (int j = B - 1; j >= 0; --j) {
+        const long long u = r < cnt[j] ? imax(xin[j], gfr[j]) - (wsuf[j] + DLs[j]) +
+                                             (dur + dl[j] + wl[j])
+                                       : kNegMP;
+        run = imax(run, u + hb[j]);
+        um[j] = run;
+      }
+      long long sc = run;
+      for (int o = 1; o < nl; o <<= 1) {  // inclusive suffix max over the owning lanes
+        const long long ov = shfl_down64(sc, o);
+        if (lane + o < nl) sc = imax(sc, ov);
+      }
+      long long above = shfl_down64(sc, 1);
+      if (lane + 1 >= nl) above = kNegMP;
       // evaluate the lane's stages; check the WAN links at their inputs
       int conf = -1;
       long long conf_y = 0;
 #pragma unroll
       for (int j = B - 1; j >= 0; --j) {
-        if (r >= cnt[j]) {
-          v = kNegMP;
-          continue;
-        }
-        lo[j] = imax(link[j] ? v : xin[j], gfr[j]);
-        v = lo[j] + dur + dl[j] + wl[j];
+        lo[j] = wsuf[j] + DLs[j] + (imax(um[j], above) - hb[j]) - (dur + dl[j] + wl[j]);
         const int w = wbi[j];
-        if (w >= 0 && conf < 0) {
+        if (r < cnt[j] && w >= 0 && conf < 0) {
           const long long y = lo[j] + dur + dl[j];
           if (link_conflict(X.mb + (size_t)w * C * M, mn[j], mcur[j], ownb[j], serb[j], y)) {
             conf = j;
@@ -400,13 +415,22 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
       const unsigned bal = __ballot_sync(kFull, conf >= 0);
       if (!bal) break;
       const int src = 31 - __clz(bal);  // topmost conflict: its input is final
+      long long shift = 0;
       if (lane == src) {
 #pragma unroll
         for (int j = 0; j < B; ++j)
-          if (j == conf)
-            dl[j] += link_fit(X.mb + (size_t)wbi[j] * C * M, X.jb + (size_t)wbi[j] * C * M, mn[j],
-                              mcur[j], ownb[j], serb[j],
-                              conf_y) - conf_y;
+          if (j == conf) {
+            shift = link_fit(X.mb + (size_t)wbi[j] * C * M, X.jb + (size_t)wbi[j] * C * M, mn[j],
+                             mcur[j], ownb[j], serb[j], conf_y) - conf_y;
+            dl[j] += shift;
+          }
+      }
+      {  // the shift enters every suffix sum at or below its stage
+        const int sw = __shfl_sync(kFull, lane * B + conf, src);
+        shift = shfl_idx64(shift, src);
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+          if (lane * B + j <= sw) DLs[j] += shift;
       }
     }
     if (cph) {
@@ -754,6 +778,27 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
 #pragma unroll
     for (int j = 0; j < B; ++j) a_loc[j] += excl;
   }
+  // wsuf[j]: sum over stages i >= s of (pair duration + WAN delay of the
+  // gradient link of i) — the cascade's single-chain suffix sums
+  long long wsuf[B];
+  {
+    long long loc = 0;
+#pragma unroll
+    for (int j = B - 1; j >= 0; --j) {
+      const int s = lane * B + j;
+      if (s < S) loc += dur + (wbi[j] >= 0 ? serb[j] + latb[j] : 0);
+      wsuf[j] = loc;
+    }
+    long long incl = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long v = shfl_down64(incl, o);
+      if (lane + o < 32) incl += v;
+    }
+    const long long excl = incl - loc;
+#pragma unroll
+    for (int j = 0; j < B; ++j) wsuf[j] += excl;
+  }
 
   // ------------------------------------------------------ forward phase
   // Per-lane registers for the current pipeline p: gpu_free and drained
@@ -822,7 +867,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
       nblk = __reduce_add_sync(kFull, nblk);
       if (nblk > 0) {
         atlas_cascade<B, TIMELINE>(g, p, m, mem_limit, X, gfr, drr, wbi, serb, latb, ownb, mcur,
-                                   mn, n_pairs, n_stage_it, n_rounds, phase ? cph : nullptr);
+                                   mn, wsuf, n_pairs, n_stage_it, n_rounds, phase ? cph : nullptr);
         ++n_adm;
       }
       if (phase) {
