@@ -267,6 +267,11 @@ int gpb_get_timing(gpb_ctx* ctx, gpb_timing* out);
  * register chains over every SM. Returns Gop/s. */
 int gpb_microbench(gpb_ctx* ctx, int32_t kind, double* gops);
 
+/* Per-bucket timing events in gpb_evaluate (default on: gpb_get_timing's
+ * policy_ms and gpb_bucket_infos' times need them; off saves ~2 event
+ * records per bucket of host launch time). */
+int gpb_set_bucket_timing(gpb_ctx* ctx, int32_t enable);
+
 /* Profiling: record each row's clock64 cost in the evaluation kernels. */
 int gpb_set_profile(gpb_ctx* ctx, int32_t enable);
 int gpb_fetch_row_cycles(gpb_ctx* ctx, int64_t* out, int64_t n);

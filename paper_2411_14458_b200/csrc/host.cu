@@ -101,6 +101,11 @@ Ctx::~Ctx() {
     if (b->ptr) cudaFree(b->ptr);
   }
   drop_graph();
+  if (upload_ev) {
+    cudaEventSynchronize(upload_ev);
+    cudaEventDestroy(upload_ev);
+  }
+  if (stage) cudaFreeHost(stage);
   if (fork_ev) cudaEventDestroy(fork_ev);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
@@ -222,6 +227,19 @@ const char* gpb_last_error(gpb_ctx* ctx) {
   return ctx ? reinterpret_cast<Ctx*>(ctx)->last_error.c_str() : "";
 }
 
+static bool same_shapes(const std::vector<Bucket>& a, const std::vector<Bucket>& b) {
+  if (a.size() != b.size()) return false;
+  for (size_t i = 0; i < a.size(); ++i) {
+    const Bucket &x = a[i], &y = b[i];
+    if (x.policy != y.policy || x.B != y.B || x.offset != y.offset || x.count != y.count ||
+        x.max_m != y.max_m || x.max_cs != y.max_cs || x.max_cm != y.max_cm ||
+        x.max_csm != y.max_csm || x.max_c != y.max_c || x.max_s != y.max_s ||
+        x.max_nw != y.max_nw || x.heavy != y.heavy)
+      return false;
+  }
+  return true;
+}
+
 int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
              const gpb_scenario* scens, int32_t n_scen, int64_t* n_rows_out) {
   if (!ctx_) return GPB_ERROR;
@@ -236,6 +254,17 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   std::vector<DevTopo> dt(std::max(n_topo, 1));
   std::vector<DevScen> ds(std::max(n_scen, 1));
   std::vector<int32_t> row_scen;
+  // single_tcp_bandwidth (libm log/exp) per distinct latency of the default
+  // calibration table: plan spaces repeat a handful of WAN latencies
+  std::vector<std::pair<double, double>> tcp_memo;
+  auto single_bw = [&](const gpb_topology& t, double lat) {
+    if (t.n_tcp > 0) return gpb_single_tcp_bandwidth(&t, lat);
+    for (const auto& kv : tcp_memo)
+      if (kv.first == lat) return kv.second;
+    const double v = gpb_single_tcp_bandwidth(&t, lat);
+    tcp_memo.emplace_back(lat, v);
+    return v;
+  };
   try {
     for (int i = 0; i < n_topo; ++i) {
       validate_topology(topos[i], i);
@@ -253,7 +282,7 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
           // latency_between (topology.cpp:21-30): symmetric by unordered pair
           const double lat = a == b ? 0.0 : t.latency_ms[std::min(a, b)][std::max(a, b)];
           d.lat_ms[a][b] = lat;
-          d.single_bw[a][b] = gpb_single_tcp_bandwidth(&t, lat);
+          d.single_bw[a][b] = single_bw(t, lat);
         }
       }
       d.pair_cap = t.pair_bw_cap;
@@ -333,6 +362,7 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
 
   // Buckets: (policy, B = ceil(S/32)); within a bucket scenarios are dealt
   // in decreasing estimated cost so the persistent warps finish together.
+  const std::vector<Bucket> prev_buckets = c.eval_ready ? c.buckets : std::vector<Bucket>();
   c.buckets.clear();
   // One bucket (one kernel) per (policy, B): rows of every shape share the
   // persistent warps, heaviest first. Estimated row cost in clock cycles
@@ -389,23 +419,47 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
     return rank(x) != rank(y) ? rank(x) < rank(y) : x.cost > y.cost;
   });
 
-  // Upload (one H2D per table).
+  // Upload: the tables are staged in one pinned buffer and copied
+  // asynchronously on the launch stream (evaluate is ordered after them).
   cudaStream_t st = c.stream;
+  const size_t sz_t = sizeof(DevTopo) * dt.size(), sz_s = sizeof(DevScen) * ds.size(),
+               sz_r = sizeof(int32_t) * row_scen.size(), sz_w = sizeof(int32_t) * work.size();
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t stage_need = al(sz_t) + al(sz_s) + al(sz_r) + al(sz_w);
+  if (c.upload_pending) {  // the previous upload must have left the staging buffer
+    cudaEventSynchronize(c.upload_ev);
+    c.upload_pending = false;
+  }
+  if (c.stage_bytes < stage_need) {
+    if (c.stage) cudaFreeHost(c.stage);
+    c.stage = nullptr;
+    c.stage_bytes = 0;
+    if (cudaMallocHost(&c.stage, stage_need) != cudaSuccess)
+      return c.cuda_fail(cudaErrorMemoryAllocation, "pinned staging");
+    c.stage_bytes = stage_need;
+  }
+  if (!c.upload_ev && cudaEventCreateWithFlags(&c.upload_ev, cudaEventDisableTiming) != cudaSuccess)
+    return c.cuda_fail(cudaGetLastError(), "event");
+  unsigned char* sp = (unsigned char*)c.stage;
   auto up = [&](Buf& b, const void* src, size_t bytes) -> bool {
     void* p = c.dev_buf(b, bytes);
     if (!p) return false;
-    return bytes == 0 || cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, st) == cudaSuccess;
+    if (bytes == 0) return true;
+    std::memcpy(sp, src, bytes);
+    const bool ok = cudaMemcpyAsync(p, sp, bytes, cudaMemcpyHostToDevice, st) == cudaSuccess;
+    sp += al(bytes);
+    return ok;
   };
-  if (!up(c.b_topos, dt.data(), sizeof(DevTopo) * dt.size()) ||
-      !up(c.b_scens, ds.data(), sizeof(DevScen) * ds.size()) ||
-      !up(c.b_row_scen, row_scen.data(), sizeof(int32_t) * row_scen.size()) ||
-      !up(c.b_work, work.data(), sizeof(int32_t) * work.size()) ||
+  if (!up(c.b_topos, dt.data(), sz_t) || !up(c.b_scens, ds.data(), sz_s) ||
+      !up(c.b_row_scen, row_scen.data(), sz_r) || !up(c.b_work, work.data(), sz_w) ||
       !c.dev_buf(c.b_rows, sizeof(gpb_row) * std::max<int64_t>(n_rows, 1)) ||
       !c.dev_buf(c.b_results, sizeof(gpb_scenario_result) * std::max(n_scen, 1)) ||
       !c.dev_buf(c.b_cursors, sizeof(int32_t) * (c.buckets.size() + 1)) ||
       !c.dev_buf(c.b_best, sizeof(gpb_best) * 1024)) {
     return c.cuda_fail(cudaGetLastError(), "upload");
   }
+  cudaEventRecord(c.upload_ev, st);
+  c.upload_pending = true;
   c.d2h_bytes = 0;
   c.h2d_bytes = sizeof(DevTopo) * dt.size() + sizeof(DevScen) * ds.size() +
                 sizeof(int32_t) * (row_scen.size() + work.size());
@@ -418,9 +472,14 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   c.dev_topos_host = dt;
   c.row_scen_host = row_scen;
   c.work_host = work;
-  c.eval_ready = false;
-  c.drop_graph();
-  if (cudaStreamSynchronize(st) != cudaSuccess) return c.cuda_fail(cudaGetLastError(), "upload");
+  // the launch sequence (ATLAS shapes, scratch, stream assignment) depends
+  // only on the buckets' shapes: reuse it when a reload has the same ones
+  if (!same_shapes(prev_buckets, c.buckets)) {
+    c.eval_ready = false;
+    c.drop_graph();
+  } else {
+    for (size_t i = 0; i < c.buckets.size(); ++i) c.buckets[i].stream = prev_buckets[i].stream;
+  }
   c.loaded = true;
   if (n_rows_out) *n_rows_out = n_rows;
   return GPB_OK;
@@ -443,13 +502,14 @@ static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
   const size_t n_side = c.n_side;
   cudaEventRecord(c.fork_ev, st);  // fork point (dependency only)
   for (size_t k = 0; k < n_side; ++k) cudaStreamWaitEvent(c.side[k], c.fork_ev, 0);
-  rec(c.bucket_ev[c.buckets.size()], st);
+  const bool bt = c.bucket_timing;  // per-bucket events (profiling, roofline)
+  if (bt) rec(c.bucket_ev[c.buckets.size()], st);
   for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
     const Bucket& b = c.buckets[bi];
     cudaStream_t ss = c.side[b.stream];
-    rec(c.bucket_ev[bi], ss);
+    if (bt) rec(c.bucket_ev[bi], ss);
     if (b.count == 0) {
-      rec(c.bucket_ev_end[bi], ss);
+      if (bt) rec(c.bucket_ev_end[bi], ss);
       continue;
     }
     EvalArgs a;
@@ -480,7 +540,7 @@ static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
       e = launch_atlas(b.B, a, P.grid, P.wpc, ss);
     }
     if (e != cudaSuccess) return c.cuda_fail(e, "eval launch");
-    rec(c.bucket_ev_end[bi], ss);
+    if (bt) rec(c.bucket_ev_end[bi], ss);
     ++launches;
   }
   for (size_t k = 0; k < n_side; ++k) {  // join
@@ -632,6 +692,7 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     if (e != cudaSuccess) return c.cuda_fail(e, "graph launch");
   }
   c.timing_valid = true;
+  c.bucket_timing_valid = c.bucket_timing;
   if (sync) {
     const cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return c.cuda_fail(e, "evaluate");
@@ -697,7 +758,10 @@ int gpb_copy_best(gpb_ctx* ctx_, void* dst) {
 int gpb_set_stream(gpb_ctx* ctx_, void* s) {
   if (!ctx_) return GPB_ERROR;
   Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
-  c.stream = s ? (cudaStream_t)s : c.own_stream;
+  cudaStream_t ns = s ? (cudaStream_t)s : c.own_stream;
+  // work on the new stream must see the last upload (async on the old one)
+  if (c.upload_pending && ns != c.stream) cudaStreamWaitEvent(ns, c.upload_ev, 0);
+  c.stream = ns;
   return GPB_OK;  // the evaluate graph is re-captured for a new stream
 }
 
@@ -729,7 +793,7 @@ int gpb_bucket_infos(gpb_ctx* ctx_, gpb_bucket_info* out, int32_t cap, int32_t* 
                                    : (d.policy == GPB_1F1B ? 4 * SM : 5 * SM) + 6 * WM;
     }
     o.algo_ops = ops;
-    if (c.timing_valid) {
+    if (c.timing_valid && c.bucket_timing_valid) {
       cudaEventElapsedTime(&o.start_ms, c.bucket_ev[c.buckets.size()], c.bucket_ev[bi]);
       cudaEventElapsedTime(&o.ms, c.bucket_ev[bi], c.bucket_ev_end[bi]);
     }
@@ -742,6 +806,14 @@ void* gpb_device_best(gpb_ctx* ctx_) {
   return reinterpret_cast<Ctx*>(ctx_)->b_best.ptr;
 }
 
+int gpb_set_bucket_timing(gpb_ctx* ctx_, int32_t enable) {
+  if (!ctx_) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  if (c.bucket_timing != (enable != 0)) c.drop_graph();
+  c.bucket_timing = enable != 0;
+  return GPB_OK;
+}
+
 int gpb_get_timing(gpb_ctx* ctx_, gpb_timing* out) {
   if (!ctx_ || !out) return GPB_ERROR;
   Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
@@ -751,7 +823,7 @@ int gpb_get_timing(gpb_ctx* ctx_, gpb_timing* out) {
     cudaEventElapsedTime(&out->evaluate_ms, c.ev0, c.ev2);
     cudaEventElapsedTime(&out->timing_kernels_ms, c.ev0, c.ev1);
     cudaEventElapsedTime(&out->select_ms, c.ev1, c.ev2);
-    for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
+    for (size_t bi = 0; c.bucket_timing_valid && bi < c.buckets.size(); ++bi) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, c.bucket_ev[bi], c.bucket_ev_end[bi]);
       out->policy_ms[c.buckets[bi].policy] += ms;

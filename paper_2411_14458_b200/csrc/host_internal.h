@@ -90,6 +90,8 @@ struct Ctx {
   int *tl_gcnt = nullptr, *tl_ghas = nullptr;
   void* tl_slots_dev = nullptr;
   bool timing_valid = false;
+  bool bucket_timing = true;         // record per-bucket events in evaluate
+  bool bucket_timing_valid = false;  // ... and the last evaluate did
   // evaluate launch sequence: prepared once per loaded space, replayed as a graph
   bool eval_ready = false;
   size_t n_side = 0;
@@ -101,6 +103,12 @@ struct Ctx {
   std::vector<size_t> scr_off;    // per bucket offset into b_scratch (int64)
   int last_launches = 0;
   float pack_ms = 0.f;
+  // pinned staging of the uploaded tables (async H2D; reused once the
+  // previous upload has left it: upload_ev)
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  cudaEvent_t upload_ev = nullptr;
+  bool upload_pending = false;
 
   std::vector<Buf*> all_bufs() {
     return {&b_topos, &b_scens, &b_row_scen, &b_work, &b_rows, &b_results, &b_cursors,

@@ -29,6 +29,8 @@
 // Right-pack (scheduler.cpp:506-529) runs only in the timeline variant.
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "atlas_layout.h"
 #include "eval_common.cuh"
 
@@ -1106,11 +1108,30 @@ __global__ void __launch_bounds__(kEvalThreads, 1) atlas_timeline_kernel(EvalArg
   }
 }
 
+// Raise a kernel's dynamic shared memory limit only when a launch needs more
+// than it was set to (per device; the attribute call costs host time on every
+// evaluate otherwise).
+template <int B, bool TL>
+static cudaError_t ensure_smem_attr(size_t smem) {
+  static std::mutex mu;
+  static int done[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && done[dev] >= (int)smem) return cudaSuccess;
+  const cudaError_t e =
+      TL ? cudaFuncSetAttribute(atlas_timeline_kernel<B>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+         : cudaFuncSetAttribute(atlas_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem);
+  if (e == cudaSuccess && dev < 64) done[dev] = (int)smem;
+  return e;
+}
+
 template <int B>
 static cudaError_t launch_atlas_tl_b(const EvalArgs& a, int grid, int wpc, cudaStream_t st) {
   const size_t smem = (size_t)wpc * a.lay.total;
-  cudaError_t e = cudaFuncSetAttribute(atlas_timeline_kernel<B>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr<B, true>(smem);
   if (e != cudaSuccess) return e;
   atlas_timeline_kernel<B><<<grid, 32 * wpc, smem, st>>>(a);
   return cudaGetLastError();
@@ -1133,8 +1154,7 @@ cudaError_t launch_atlas_timeline(int B, const EvalArgs& a, int grid, int wpc, c
 template <int B>
 static cudaError_t launch_atlas_b(const EvalArgs& a, int grid, int wpc, cudaStream_t st) {
   const size_t smem = (size_t)wpc * a.lay.total;
-  cudaError_t e = cudaFuncSetAttribute(atlas_kernel<B>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr<B, false>(smem);
   if (e != cudaSuccess) return e;
   atlas_kernel<B><<<grid, 32 * wpc, smem, st>>>(a);
   return cudaGetLastError();
@@ -1146,10 +1166,7 @@ int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem) {
   cudaError_t e = cudaSuccess;
 #define GPB_OCC(BB)                                                                         \
   case BB:                                                                                  \
-    e = timeline ? cudaFuncSetAttribute(atlas_timeline_kernel<BB>,                          \
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) \
-                 : cudaFuncSetAttribute(atlas_kernel<BB>,                                   \
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    e = timeline ? ensure_smem_attr<BB, true>(smem) : ensure_smem_attr<BB, false>(smem);      \
     if (e == cudaSuccess)                                                                   \
       e = timeline ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_timeline_kernel<BB>, \
                                                                    32 * wpc, smem)          \

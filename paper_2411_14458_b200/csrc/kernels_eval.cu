@@ -421,13 +421,16 @@ __global__ void best_reduce_kernel(const gpb_best* in, int n, gpb_best* out) {
 template <int B>
 static cudaError_t launch_flush_b(bool gpipe, const EvalArgs& a, int grid, cudaStream_t st) {
   const size_t smem = (size_t)(kEvalThreads / 32) * a.smem_m * sizeof(long long);
+  // (above the default 48 KB only: the attribute call costs host time per launch)
   if (gpipe) {
-    cudaFuncSetAttribute(flush_kernel<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(flush_kernel<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
     flush_kernel<B, true><<<grid, kEvalThreads, smem, st>>>(a);
   } else {
-    cudaFuncSetAttribute(flush_kernel<B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(flush_kernel<B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
     flush_kernel<B, false><<<grid, kEvalThreads, smem, st>>>(a);
   }
   return cudaGetLastError();

@@ -77,6 +77,7 @@ def load_library(path: str = LIB_PATH):
         "gpb_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
         "gpb_copy_best": (C.c_int, [C.c_void_p, C.c_void_p]),
         "gpb_set_profile": (C.c_int, [C.c_void_p, C.c_int32]),
+        "gpb_set_bucket_timing": (C.c_int, [C.c_void_p, C.c_int32]),
         "gpb_set_allreduce_tail": (C.c_int, [C.c_void_p, C.c_int32]),
         "gpb_timeline_arrays": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_int64), P(C.c_int64),
                                           C.c_int64, P(C.c_int32), P(C.c_int64)]),
@@ -98,7 +99,8 @@ def exported_symbols():
             "gpb_fetch_best", "gpb_device_best", "gpb_bubbles", "gpb_pack_prefills",
             "gpb_synthetic_requests", "gpb_get_timing", "gpb_microbench", "gpb_set_stream",
             "gpb_copy_best", "gpb_set_profile", "gpb_fetch_row_cycles",
-            "gpb_set_allreduce_tail", "gpb_timeline_arrays", "gpb_bucket_infos"]
+            "gpb_set_allreduce_tail", "gpb_timeline_arrays", "gpb_bucket_infos",
+            "gpb_set_bucket_timing"]
 
 
 @dataclass
@@ -178,6 +180,9 @@ class Planner:
 
     def set_stream(self, cuda_stream: int | None):
         self._check(self.lib.gpb_set_stream(self.ctx, cuda_stream or None))
+
+    def set_bucket_timing(self, enable: bool):
+        self._check(self.lib.gpb_set_bucket_timing(self.ctx, int(bool(enable))))
 
     def set_profile(self, enable: bool):
         self._check(self.lib.gpb_set_profile(self.ctx, int(bool(enable))))
