@@ -780,6 +780,12 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
 #pragma unroll
     for (int j = 0; j < B; ++j) a_loc[j] += excl;
   }
+  // chain offsets of the stages before each WAN boundary (lane w reads a_w)
+#pragma unroll
+  for (int j = 0; j < B; ++j)
+    if (wfi[j] >= 0) X.wa[wfi[j]] = a_loc[j];
+  const int wsrc = lane < nw ? g.blk_first[lane + 1] - 1 : lane;  // B == 1: that stage's lane
+  __syncwarp();
   // wsuf[j]: sum over stages i >= s of (pair duration + WAN delay of the
   // gradient link of i) — the cascade's single-chain suffix sums
   long long wsuf[B];
@@ -852,6 +858,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     const int* jgw_l = nullptr;
     int nmw_l = 0;
     if (lane < nw) {
+      aw_l = X.wa[lane];
       lenw_l = X.wa[8 + lane];
       mgw_l = X.mf + (size_t)lane * C * M;
       jgw_l = X.jf + (size_t)lane * C * M;
@@ -886,23 +893,25 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
         gl[j] = runmax;
       }
       long long pre = runmax;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
+      for (int o = 1; o < nl; o <<= 1) {  // warp-uniform trip count
         const long long v = shfl_up64(pre, o);
         if (lane >= o) pre = imax(pre, v);
       }
       long long prev = shfl_up64(pre, 1);
       if (lane == 0) prev = -kInf64;
+      long long gw = 0;  // lane w: G of the stage before WAN boundary w
 #pragma unroll
-      for (int j = 0; j < B; ++j) {
-        gl[j] = imax(gl[j], prev);
-        if (wfi[j] >= 0) {
-          X.wa[wfi[j]] = a_loc[j];
-          X.wg[wfi[j]] = gl[j];
-        }
+      for (int j = 0; j < B; ++j) gl[j] = imax(gl[j], prev);
+      if (B == 1) {  // that stage is lane wsrc's only stage
+        gw = shfl_idx64(gl[0], wsrc);
+      } else {
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+          if (wfi[j] >= 0) X.wg[wfi[j]] = gl[j];
+        __syncwarp();
+        if (lane < nw) gw = X.wg[lane];
       }
       long long t0 = __shfl_sync(kFull, gfr[0], 0);  // gpu_free of stage 0
-      __syncwarp();
       if (phase) {
         const long long t1 = clock64();
         ph_chain += t1 - ph_t;
@@ -913,11 +922,6 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
       // (lane w checks link w; the lowest conflicting link shifts t0, as the
       // reference's restart from stage 0 does)
       if (nw > 0) {
-        long long gw = 0;
-        if (lane < nw) {
-          aw_l = X.wa[lane];
-          gw = X.wg[lane];
-        }
         for (;;) {
           const long long e = aw_l + f + imax(t0, gw);
           const bool conf = lane < nw && link_conflict(mgw_l, nmw_l, curf, ownw_l, lenw_l, e);

@@ -101,3 +101,49 @@ def test_best_is_global_argmax(planner):
     if cand:
         thr, neg = max(cand)
         assert best.row == -neg and best.throughput == thr
+
+
+def test_reload_same_shapes_and_stream_switch(planner, checker):
+    """A reload with the same bucket shapes keeps the prepared launch sequence
+    (host.cu gpb_load); uploads are asynchronous on the launch stream, and a
+    stream switch after the load must still see them. Every row stays
+    bit-exact with the reference."""
+    import ctypes
+
+    import torch
+    from oracle import bindings
+
+    def clone(x):
+        y = type(x)()
+        ctypes.memmove(ctypes.byref(y), ctypes.byref(x), ctypes.sizeof(x))
+        return y
+
+    topos, scens = random_space(4321, 120, wide=False)
+    assert _compare_space(planner, checker, bindings.port(), topos, scens) > 120
+    # same shapes (policy, stages, microbatches, pipelines, row counts),
+    # different WAN latencies and compute times
+    topos2 = abi.array(abi.Topology, [clone(t) for t in topos])
+    for t in topos2:
+        for a in range(t.n_dc):
+            for b in range(t.n_dc):
+                if a != b:
+                    t.latency_ms[a][b] = t.latency_ms[a][b] * 1.5 + 3.0
+    scens2 = abi.array(abi.Scenario, [clone(s) for s in scens])
+    for s in scens2:
+        s.fwd_ms, s.bwd_ms = s.fwd_ms * 1.25, s.bwd_ms * 0.8
+        if s.ratio_C > 0:
+            s.ratio_C = s.ratio_C * 0.75
+    assert _compare_space(planner, checker, bindings.port(), topos2, scens2) > 120
+    # load on the own stream, evaluate on a fresh torch stream
+    side = torch.cuda.Stream()
+    planner.set_stream(None)
+    planner.load(topos, scens)
+    planner.set_stream(side.cuda_stream)
+    planner.evaluate()
+    rows = planner.rows()
+    planner.set_stream(None)
+    for i, sc in enumerate(scens[:40]):
+        ref_rows, _, _ = checker.select(topos, sc)
+        r0 = planner.scenario_results()[i].first_row
+        for a, b in zip(rows[r0:r0 + len(ref_rows)], ref_rows):
+            assert _row_key(a) == _row_key(b)
