@@ -103,5 +103,59 @@ def config3(n_rows=1_000_000, seed=2, shard=0, n_shards=1):
     return topos, scens
 
 
+# (name, layers, hidden, seq_len): GPT-A / GPT-B are the paper's baseline
+# models (L,H = 4K,4K and 6K,8K; their layer counts are not
+# given there: 24 and 48 here), Llama-3 70B and Llama-3.1 405B as above.
+CONFIG5_MODELS = [("gpt-a", 24, 4096, 4096), ("gpt-b", 48, 8192, 6144),
+                  ("llama3-70b", 80, 8192, 8192), ("llama3.1-405b", 126, 16384, 8192)]
+
+
+def config5(n_rows=10_000_000, seed=5, shard=0, n_shards=1, max_rows_per_scenario=0):
+    """Config 5: the full sweep — random topologies of 2-8 DCs with
+    64..1024 GPUs each (step 64), the four models, microbatches 4-256, and
+    every other axis of config 3; `shard` selects every n_shards-th scenario.
+    `max_rows_per_scenario` > 0 caps each scenario's D range (parity samples)."""
+    lat_axis = [5.0, 10.0, 20.0, 40.0, 80.0, 160.0]
+    cap_axis = [1.0, 2.5, 5.0, 10.0, 25.0]
+    lpp_axis = [1, 2, 3, 4, 6, 8, 12, 16]
+    C_axis = [1, 2, 3, 4]
+    tp_axis = [1, 2, 4, 8]
+    M_axis = [4, 8, 16, 32, 64, 128, 256]
+    ratio_axis = [1.0, 2.0, 3.0]
+    rng = random.Random(seed)
+    topos, scens, rows, k = [], [], 0, 0
+    while rows < n_rows:
+        pick = lambda axis: axis[rng.randrange(len(axis))]  # noqa: E731
+        n_dc = 2 + rng.randrange(7)
+        counts = [64 * (1 + rng.randrange(16)) for _ in range(n_dc)]
+        lat = [[0.0] * n_dc for _ in range(n_dc)]
+        for i in range(n_dc):
+            for j in range(i + 1, n_dc):
+                lat[i][j] = lat[j][i] = pick(lat_axis)
+        cap = pick(cap_axis)
+        _, layers, hidden, seq = pick(CONFIG5_MODELS)
+        lpp, C, tp, M = pick(lpp_axis), pick(C_axis), pick(tp_axis), pick(M_axis)
+        ratio, pol, multi = pick(ratio_axis), pick(POLICY_LIST), pick([0, 1])
+        order = list(range(n_dc))
+        rng.shuffle(order)
+        P = (layers + lpp - 1) // lpp
+        d_max = _d_max_default(counts, C, P, tp)
+        if max_rows_per_scenario > 0:
+            d_max = min(d_max, max_rows_per_scenario)
+        if rows + d_max > n_rows:
+            d_max = n_rows - rows
+        rows += d_max
+        mine = k % n_shards == shard
+        k += 1
+        if not mine:
+            continue
+        topos.append(abi.make_topology(counts, cap_gbps=cap, intra_gbps=100.0, latency=lat))
+        scens.append(abi.make_scenario(
+            topology=len(topos) - 1, policy=pol, num_layers=layers, layers_per_partition=lpp,
+            num_microbatches=M, hidden=hidden, seq_len=seq, ratio_C=ratio, C=C, tp=tp,
+            d_max=d_max, dc_order=order, multi_conn=multi))
+    return topos, scens
+
+
 def count_rows(scens):
     return sum(s.d_max for s in scens)

@@ -1,0 +1,37 @@
+"""GPU parity on BASELINE config 5's shapes (workloads.config5): random
+topologies of 2-8 DCs, GPT-A/GPT-B/70B/405B, microbatches 4-256, every
+policy — all rows bit-exact with the reference (oracle/_ref), plus the
+largest ATLAS cell the sweep holds (405B at one layer per stage: 126 stages,
+8 DCs, 4 pipelines, 256 microbatches)."""
+import pytest
+
+from paper_2411_14458_b200 import abi, workloads
+from tests.test_gpu_rows import _compare_space
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_config5_sample_bit_exact(planner, checker, seed):
+    from oracle import bindings
+    topos, scens = workloads.config5(1500, seed=seed, max_rows_per_scenario=3)
+    topos = abi.array(abi.Topology, topos)
+    assert {t.n_dc for t in topos} >= {2, 8}
+    assert max(s.num_microbatches for s in scens) == 256
+    assert _compare_space(planner, checker, bindings.port(), topos, scens) == 1500
+
+
+def test_config5_largest_atlas_cell(planner, checker):
+    from oracle import bindings
+    n = 8
+    lat = [[0.0 if i == j else 10.0 * (1 + abs(i - j)) for j in range(n)] for i in range(n)]
+    topo = abi.make_topology([1024, 896, 768, 640, 512, 384, 256, 128], cap_gbps=5.0, latency=lat)
+    scens = []
+    for pol in ("atlas", "gpipe", "1f1b", "varuna"):
+        for multi in (0, 1):
+            scens.append(abi.make_scenario(
+                topology=0, policy=pol, num_layers=126, layers_per_partition=1,
+                num_microbatches=256, hidden=16384, seq_len=8192, ratio_C=2.0, C=4, tp=1,
+                d_max=2, dc_order=list(range(n)), multi_conn=multi))
+    topos = abi.array(abi.Topology, [topo])
+    assert _compare_space(planner, checker, bindings.port(), topos, scens) == 2 * len(scens)
