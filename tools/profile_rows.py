@@ -9,7 +9,7 @@ from paper_2411_14458_b200 import abi, workloads  # noqa: E402
 from paper_2411_14458_b200.planner import Planner  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "config2"
-topos, scens = getattr(workloads, cfg)()
+topos, scens = getattr(workloads, cfg)(**({"n_rows": int(sys.argv[3])} if len(sys.argv) > 3 else {}))
 p = Planner(0)
 p.set_profile(True)
 n = p.load(abi.array(abi.Topology, topos), abi.array(abi.Scenario, scens))
@@ -35,6 +35,10 @@ for r, c, ph in zip(rows[:n], cyc, phase):
         for k in range(16):
             a[3][k] += ph[k]
 tot = sum(v[1] for v in agg.values())
+by_pol = collections.Counter()
+for k, v in agg.items():
+    by_pol[k[0]] += v[1]
+print("cycles by policy:", {k: f"{100 * v / tot:.1f}%" for k, v in by_pol.most_common()})
 print(json.dumps({"evaluate_ms": t.evaluate_ms, "policy_ms": list(t.policy_ms)}))
 print("policy S C M feas | rows  sum_Mcyc  share  max_kcyc")
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:int(sys.argv[2]) if len(sys.argv) > 2 else 25]:
