@@ -582,18 +582,21 @@ __device__ __forceinline__ void group_caps(const PackArgs& a, const TlSlot& sl, 
   }
 }
 
-// One warp per plan runs the FCFS request loop (schedule_prefills,
-// bubbletea.cpp:132-222). Requests are staged 32 at a time (one per lane:
-// load, durations, arrival check); a request is examined only if it passes
-// the warp-wide bound (some pipeline's caps admit its durations). The lanes
-// then filter 32 pipelines at a time by their caps and hand the survivors,
-// in pipeline order, to groups of lanes that search them concurrently;
-// first fit = the lowest feasible pipeline.
-__global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
+// One CTA of kPackWarps warps per plan runs the FCFS request loop
+// (schedule_prefills, bubbletea.cpp:132-222). Requests are staged 32 per warp
+// (one per lane: load, durations, arrival check) and searched speculatively
+// by every warp at once on the batch-start state (phase 1); warp 0 then
+// resolves the batch in FCFS order and commits (phase 2). A request is
+// examined only if it passes the plan-wide bound (some pipeline's caps admit
+// its durations).
+constexpr int kPackWarps = 4;
+
+__global__ void __launch_bounds__(32 * kPackWarps, 1) pack_kernel(PackArgs a) {
   extern __shared__ __align__(16) long long pk_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int si = blockIdx.x * (blockDim.x >> 5) + warp;
+  constexpr int BW = 32 * kPackWarps;  // requests per batch
+  const int si = blockIdx.x;
   if (si >= a.n_slots) return;
   const TlSlot& sl = a.slots[si];
   const long long H = a.hz[si];
@@ -609,13 +612,25 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
   while (gs < d_eff && gs < 32) gs <<= 1;
   const int ng = 32 / gs, grp = lane / gs, gl = lane & (gs - 1);
   unsigned* memo = a.memo + (size_t)si * a.max_pipes * a.memo_words;
-  long long* capA = pk_smem + (size_t)warp * 2 * a.max_pipes;
+  // shared: caps per pipeline, the batch table, per-batch "committed" flags
+  long long* capA = pk_smem;
   long long* capB = capA + a.max_pipes;
-  // per-batch "committed" flag per pipeline
-  unsigned char* cflag = (unsigned char*)(pk_smem + (size_t)(blockDim.x >> 5) * 2 * a.max_pipes) +
-                         (size_t)warp * a.max_pipes;
-  for (int i = lane; i < G; i += 32) a.gpu_off[gb + i] = -1;
-  __syncwarp();
+  long long* tb_arr = capB + a.max_pipes;  // [BW] arrival
+  long long* tb_d0 = tb_arr + BW;
+  long long* tb_d1 = tb_d0 + BW;
+  long long* tb_ovh = tb_d1 + BW;
+  long long* tb_t1 = tb_ovh + BW;          // phase-1 start
+  long long* tb_rstart = tb_t1 + BW;       // committed start (phase 2)
+  unsigned long long* tb_fail = (unsigned long long*)(tb_rstart + BW);
+  long long* tb_bound = (long long*)(tb_fail + BW);  // [0] max capA, [1] max capB
+  int* tb_pipe1 = (int*)(tb_bound + 2);
+  int* tb_rpipe = tb_pipe1 + BW;
+  int* tb_tok = tb_rpipe + BW;
+  int* tb_id = tb_tok + BW;
+  int* tb_stop = tb_id + BW;  // pool overflow: every warp leaves
+  unsigned char* cflag = (unsigned char*)(tb_stop + 4);
+  for (int i = threadIdx.x; i < G; i += blockDim.x) a.gpu_off[gb + i] = -1;
+  if (threadIdx.x == 0) *tb_stop = 0;
   const long long pool_base = (long long)si * a.pool_per_slot;
   long long bump = 0;
   const int total_layers = max(1, base_l * D + extra);
@@ -624,29 +639,38 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
   long long st_exam = 0, st_search = 0, st_fail = 0, st_iter = 0, st_cyc_search = 0,
             st_cyc_caps = 0, st_cyc_commit = 0;
   const long long st_t0 = clock64();
+  __syncthreads();
   // initial caps, at the earliest arrival
   const long long a0 = a.n_req > 0 ? a.sufmin[0] : 0;
-  for (int p0 = 0; p0 < n_pipes; p0 += ng) {
-    const int pi = p0 + grp < n_pipes ? p0 + grp : -1;
-    long long ca, cb;
-    group_caps(a, sl, gb, pi, a0, extra, gs, ca, cb, zrun);
-    if (pi >= 0 && gl == 0) {
-      capA[pi] = ca;
-      capB[pi] = cb;
+  if (warp == 0) {
+    for (int p0 = 0; p0 < n_pipes; p0 += ng) {
+      const int pi = p0 + grp < n_pipes ? p0 + grp : -1;
+      long long ca, cb;
+      group_caps(a, sl, gb, pi, a0, extra, gs, ca, cb, zrun);
+      if (pi >= 0 && gl == 0) {
+        capA[pi] = ca;
+        capB[pi] = cb;
+      }
+    }
+    __syncwarp();
+    long long mA = -kInf64, mB = -kInf64;
+    for (int pi = lane; pi < n_pipes; pi += 32) {
+      mA = max(mA, capA[pi]);
+      mB = max(mB, capB[pi]);
+    }
+    mA = warp_max64(mA);
+    mB = warp_max64(mB);
+    if (lane == 0) {
+      tb_bound[0] = mA;
+      tb_bound[1] = mB;
     }
   }
-  __syncwarp();
-  long long mA = -kInf64, mB = -kInf64;
-  for (int pi = lane; pi < n_pipes; pi += 32) {
-    mA = max(mA, capA[pi]);
-    mB = max(mB, capB[pi]);
-  }
-  mA = warp_max64(mA);
-  mB = warp_max64(mB);
-  for (long long r0 = 0; r0 < a.n_req; r0 += 32) {
-    // stage 32 requests: durations (prefill_duration_ms :68-76, transfer
-    // :78-86, per-stage split :154-161)
-    const long long r = r0 + lane;
+  __syncthreads();
+  for (long long r0 = 0; r0 < a.n_req; r0 += BW) {
+    // stage 32 requests per warp: durations (prefill_duration_ms :68-76,
+    // transfer :78-86, per-stage split :154-161)
+    const int jb = warp * 32 + lane;  // index in the batch
+    const long long r = r0 + jb;
     gpb_request q{};
     long long arrival = kInf64;
     ReqGeom rg{0, 0, 0, extra};
@@ -667,10 +691,7 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
       }
     }
     const bool in_range = r < a.n_req;
-    const unsigned todo0 = __ballot_sync(kFull, live && rg.d0 <= mB && (extra == 0 || rg.d1 <= mA));
-    unsigned won = 0;
-    long long my_start = -1;
-    int my_pipe = -1;
+    const long long mA = tb_bound[0], mB = tb_bound[1];
     // Phase 1 — every staged request searches the batch-start state at once
     // (lane = request, pipelines in order, its stages checked with independent
     // loads). Commits only shrink gap lists and only on the committing
@@ -678,7 +699,7 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
     // infeasible for the rest of the batch, and a request's answer (pipeline,
     // earliest start) stays exact unless an earlier request of the batch
     // committed to that same pipeline (phase 2 re-searches those).
-    const bool act = (todo0 >> lane) & 1u;
+    const bool act = live && rg.d0 <= mB && (extra == 0 || rg.d1 <= mA);
     const int tok_l = q.tokens - 1;
     int pi_l = act ? 0 : n_pipes;
     int pipe1 = -1;
@@ -712,70 +733,84 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
       }
       st_cyc_search += clock64() - tc;
     }
-    for (int i = lane; i < n_pipes; i += 32) cflag[i] = 0;
-    __syncwarp();
-    // Phase 2 — FCFS over the batch: commit each answer whose pipeline no
-    // earlier request of the batch took; otherwise search again from that
-    // pipeline on (warp-cooperative, lane groups over pipelines).
-    unsigned res = __ballot_sync(kFull, pipe1 >= 0);
-    while (res) {
-      ++st_exam;
-      const int src = __ffs(res) - 1;
-      res &= res - 1;
-      int win = __shfl_sync(kFull, pipe1, src);
-      long long win_t = shfl_idx64(t1, src);
-      const long long a_ref = a.sufmin[r0 + src];  // <= every arrival from here on
-      ReqGeom g2;
-      g2.d0 = shfl_idx64(rg.d0, src);
-      g2.d1 = shfl_idx64(rg.d1, src);
-      g2.ovh = shfl_idx64(rg.ovh, src);
-      g2.extra = extra;
-      if (cflag[win]) {
-        const long long tc = clock64();
-        const int from = win;
-        const long long arr = shfl_idx64(arrival, src);
-        const int tok = __shfl_sync(kFull, q.tokens, src) - 1;
-        win = -1;
-        for (int c0 = from & ~31; c0 < n_pipes && win < 0; c0 += 32) {
-          const int pl = c0 + lane;
-          bool cand = pl >= from && pl < n_pipes && g2.d0 <= capB[pl] &&
-                      (extra == 0 || g2.d1 <= capA[pl]);
-          if (cand) cand = !((memo[(size_t)pl * a.memo_words + (tok >> 5)] >> (tok & 31)) & 1u);
-          unsigned pmask = __ballot_sync(kFull, cand);
-          while (pmask && win < 0) {
-            // the next ng survivors, in pipeline order, one per group
-            const unsigned bit = __fns(pmask, 0, grp + 1);
-            const int pi = bit < 32 ? c0 + (int)bit : -1;
-            st_search += pi >= 0 && gl == 0;
-            const long long t = group_search<4>(a, sl, gb, pi, arr, g2, gs, st_iter, zrun);
-            const unsigned ok = __ballot_sync(kFull, gl == 0 && pi >= 0 && t != kInf64);
-            if (ok) {
-              const int wl = __ffs(ok) - 1;  // lowest group = lowest pipeline
-              win = __shfl_sync(kFull, pi, wl);
-              win_t = shfl_idx64(t, wl);
-            }
-            // failed searches below the winner (or all): tighten their caps
-            const bool failed = pi >= 0 && t == kInf64 && (win < 0 || pi < win);
-            st_fail += failed && gl == 0;
-            // no start >= arr exists for this token count; every later request
-            // arrives at or after arr when arr is the minimum of the rest
-            if (failed && gl == 0 && arr == a_ref)
-              atomicOr(&memo[(size_t)pi * a.memo_words + (tok >> 5)], 1u << (tok & 31));
-            if (__any_sync(kFull, failed)) {
-              long long ca, cb;
-              group_caps(a, sl, gb, failed ? pi : -1, a_ref, extra, gs, ca, cb, zrun);
-              if (failed && gl == 0) {
-                capA[pi] = ca;
-                capB[pi] = cb;
+    tb_arr[jb] = arrival;
+    tb_d0[jb] = rg.d0;
+    tb_d1[jb] = rg.d1;
+    tb_ovh[jb] = rg.ovh;
+    tb_t1[jb] = t1;
+    tb_fail[jb] = failm;
+    tb_pipe1[jb] = pipe1;
+    tb_rpipe[jb] = -1;
+    tb_tok[jb] = tok_l;
+    tb_id[jb] = q.id;
+    __syncthreads();
+    // Phase 2 (warp 0) — FCFS over the batch: commit each answer whose
+    // pipeline no earlier request of the batch took; otherwise search again
+    // from that pipeline on (warp-cooperative, lane groups over pipelines).
+    if (warp == 0) {
+      for (int i = lane; i < n_pipes; i += 32) cflag[i] = 0;
+      __syncwarp();
+      for (int w0 = 0; w0 < BW; w0 += 32) {
+        if (*tb_stop) break;
+        unsigned res = __ballot_sync(kFull, tb_pipe1[w0 + lane] >= 0);
+        while (res && !*tb_stop) {
+          ++st_exam;
+          const int src = w0 + __ffs(res) - 1;
+          res &= res - 1;
+          int win = tb_pipe1[src];
+          long long win_t = tb_t1[src];
+          const long long a_ref = a.sufmin[r0 + src];  // <= every arrival from here on
+          ReqGeom g2;
+          g2.d0 = tb_d0[src];
+          g2.d1 = tb_d1[src];
+          g2.ovh = tb_ovh[src];
+          g2.extra = extra;
+          if (cflag[win]) {
+            const long long tc = clock64();
+            const int from = win;
+            const long long arr = tb_arr[src];
+            const int tok = tb_tok[src];
+            win = -1;
+            for (int c0 = from & ~31; c0 < n_pipes && win < 0; c0 += 32) {
+              const int pl = c0 + lane;
+              bool cand = pl >= from && pl < n_pipes && g2.d0 <= capB[pl] &&
+                          (extra == 0 || g2.d1 <= capA[pl]);
+              if (cand) cand = !((memo[(size_t)pl * a.memo_words + (tok >> 5)] >> (tok & 31)) & 1u);
+              unsigned pmask = __ballot_sync(kFull, cand);
+              while (pmask && win < 0) {
+                // the next ng survivors, in pipeline order, one per group
+                const unsigned bit = __fns(pmask, 0, grp + 1);
+                const int pi = bit < 32 ? c0 + (int)bit : -1;
+                st_search += pi >= 0 && gl == 0;
+                const long long t = group_search<4>(a, sl, gb, pi, arr, g2, gs, st_iter, zrun);
+                const unsigned ok = __ballot_sync(kFull, gl == 0 && pi >= 0 && t != kInf64);
+                if (ok) {
+                  const int wl = __ffs(ok) - 1;  // lowest group = lowest pipeline
+                  win = __shfl_sync(kFull, pi, wl);
+                  win_t = shfl_idx64(t, wl);
+                }
+                // failed searches below the winner (or all): tighten their caps
+                const bool failed = pi >= 0 && t == kInf64 && (win < 0 || pi < win);
+                st_fail += failed && gl == 0;
+                // no start >= arr exists for this token count; every later request
+                // arrives at or after arr when arr is the minimum of the rest
+                if (failed && gl == 0 && arr == a_ref)
+                  atomicOr(&memo[(size_t)pi * a.memo_words + (tok >> 5)], 1u << (tok & 31));
+                if (__any_sync(kFull, failed)) {
+                  long long ca, cb;
+                  group_caps(a, sl, gb, failed ? pi : -1, a_ref, extra, gs, ca, cb, zrun);
+                  if (failed && gl == 0) {
+                    capA[pi] = ca;
+                    capB[pi] = cb;
+                  }
+                }
+                for (int g = 0; g < ng && pmask; ++g) pmask &= pmask - 1;
               }
             }
-            for (int g = 0; g < ng && pmask; ++g) pmask &= pmask - 1;
+            st_cyc_caps += clock64() - tc;
           }
-        }
-        st_cyc_caps += clock64() - tc;
-      }
-      __syncwarp();
-      const long long tcm = clock64();
+          __syncwarp();
+          const long long tcm = clock64();
       if (win >= 0) {
         // commit (bubbletea.cpp:189-215): split the gap on each stage GPU,
         // one lane per stage GPU; copy-on-write lists come from the slot's
@@ -840,23 +875,26 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
           }
           __syncwarp();
         }
-        if (ovf) {
-          if (lane == 0) atomicExch(a.overflow, 1);
-          return;
+        if (ovf) {  // the whole CTA stops after this batch
+          if (lane == 0) {
+            atomicExch(a.overflow, 1);
+            *tb_stop = 1;
+          }
+          __syncwarp();
+          break;
         }
         ++accepted;
-        const int id = __shfl_sync(kFull, q.id, src);
+        const int id = tb_id[src];
         if (lane == 0) {
           hash = fnv_mix(hash, (unsigned long long)(long long)id);
           hash = fnv_mix(hash, (unsigned long long)(long long)win);
           hash = fnv_mix(hash, (unsigned long long)win_t);
           cflag[win] = 1;
         }
-        if (lane == src) {
-          my_pipe = win;
-          my_start = win_t;
+        if (lane == 0) {
+          tb_rpipe[src] = win;
+          tb_rstart[src] = win_t;
         }
-        won |= 1u << src;
         {  // the winner's GPU lists changed: its caps now
           long long ca, cb;
           group_caps(a, sl, gb, grp == 0 ? win : -1, a_ref, extra, gs, ca, cb, zrun);
@@ -866,57 +904,69 @@ __global__ void __launch_bounds__(128, 1) pack_kernel(PackArgs a) {
           }
         }
       }
-      __syncwarp();
-      st_cyc_commit += clock64() - tcm;
+          __syncwarp();
+          st_cyc_commit += clock64() - tcm;
+        }
+      }
     }
-    // Phase-1 failures, recorded now that the batch is resolved: the memo
-    // (a failure at the minimum remaining arrival holds for every later
-    // request with that token count) and the failed pipelines' caps at the
-    // next batch's reference time.
+    __syncthreads();
+    if (*tb_stop) return;
+    // every warp: its requests' placements; the phase-1 failures into the
+    // memo (a failure at the minimum remaining arrival holds for every later
+    // request with that token count)
+    if (a.pl && in_range) {
+      gpb_placement& o = a.pl[(size_t)si * a.n_req + r];
+      const int wp = tb_rpipe[jb];
+      const bool ok = wp >= 0;
+      o.start_ns = ok ? tb_rstart[jb] : -1;
+      o.ttft_overhead_ms = ok && D - 1 != 0 ? __dmul_rn((double)(D - 1), xfer) : 0.0;
+      o.accepted = ok ? 1 : 0;
+      o.pipeline = ok ? wp : -1;
+    }
     if (act && failm && arrival == a.sufmin[r]) {
       for (unsigned long long m = failm; m; m &= m - 1) {
         const int pi = __ffsll((long long)m) - 1;
         atomicOr(&memo[(size_t)pi * a.memo_words + (tok_l >> 5)], 1u << (tok_l & 31));
       }
     }
-    if (r0 + 32 < a.n_req) {
-      unsigned long long um = failm;
-      for (int o = 16; o > 0; o >>= 1) um |= __shfl_xor_sync(kFull, um, o);
-      const long long a_next = a.sufmin[r0 + 32];
-      while (um) {
-        // the next ng failed pipelines, one per group
-        unsigned long long mm = um;
-        for (int g = 0; g < grp && mm; ++g) mm &= mm - 1;
-        const int pi = mm ? __ffsll((long long)mm) - 1 : -1;
-        long long ca, cb;
-        group_caps(a, sl, gb, pi, a_next, extra, gs, ca, cb, zrun);
-        if (pi >= 0 && gl == 0) {
-          capA[pi] = ca;
-          capB[pi] = cb;
+    // warp 0: the failed pipelines' caps at the next batch's reference time,
+    // then the plan-wide bounds
+    if (warp == 0) {
+      if (r0 + BW < a.n_req) {
+        unsigned long long um = 0;
+        for (int i = lane; i < BW; i += 32) um |= tb_fail[i];
+        for (int o = 16; o > 0; o >>= 1) um |= __shfl_xor_sync(kFull, um, o);
+        const long long a_next = a.sufmin[r0 + BW];
+        while (um) {
+          // the next ng failed pipelines, one per group
+          unsigned long long mm = um;
+          for (int g = 0; g < grp && mm; ++g) mm &= mm - 1;
+          const int pi = mm ? __ffsll((long long)mm) - 1 : -1;
+          long long ca, cb;
+          group_caps(a, sl, gb, pi, a_next, extra, gs, ca, cb, zrun);
+          if (pi >= 0 && gl == 0) {
+            capA[pi] = ca;
+            capB[pi] = cb;
+          }
+          for (int g = 0; g < ng && um; ++g) um &= um - 1;
         }
-        for (int g = 0; g < ng && um; ++g) um &= um - 1;
       }
-    }
-    __syncwarp();
-    {  // caps only shrink: refresh the warp bounds
+      __syncwarp();
       long long ma = -kInf64, mb = -kInf64;
       for (int pi = lane; pi < n_pipes; pi += 32) {
         ma = max(ma, capA[pi]);
         mb = max(mb, capB[pi]);
       }
-      mA = warp_max64(ma);
-      mB = warp_max64(mb);
+      ma = warp_max64(ma);
+      mb = warp_max64(mb);
+      if (lane == 0) {
+        tb_bound[0] = ma;
+        tb_bound[1] = mb;
+      }
     }
-    if (a.pl && in_range) {
-      gpb_placement& o = a.pl[(size_t)si * a.n_req + r];
-      const bool ok = (won >> lane) & 1u;
-      o.start_ns = ok ? my_start : -1;
-      o.ttft_overhead_ms = ok && D - 1 != 0 ? __dmul_rn((double)(D - 1), xfer) : 0.0;
-      o.accepted = ok ? 1 : 0;
-      o.pipeline = ok ? my_pipe : -1;
-    }
-    __syncwarp();
+    __syncthreads();
   }
+  if (warp != 0) return;
   const long long rejected = a.n_req - accepted;
   if (a.stats) {
     st_search = (long long)__reduce_add_sync(kFull, (unsigned)st_search);
@@ -1386,7 +1436,9 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
     int max_pipes = 1;
     for (const TlSlot& sl2 : slots) max_pipes = std::max(max_pipes, sl2.C * sl2.S);
     a.max_pipes = max_pipes;
-    const size_t psmem = 4 * (2 * sizeof(long long) + 1) * (size_t)max_pipes;
+    // caps, batch table, flags (pack_kernel's shared layout)
+    const size_t psmem = 16 * (size_t)max_pipes + (7 * 8 + 16 + 4 * 4) * (size_t)(32 * kPackWarps) +
+                         16 + 16 + (size_t)max_pipes + 16;
     if (psmem > (size_t)c.smem_optin) {
       c.set_error("too many prefill pipelines per plan for the packing kernel");
       return GPB_CONFIG_ERROR;
@@ -1403,7 +1455,7 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
       cudaMemsetAsync(a.stats, 0, 64 * (size_t)std::max(1, n_rows_sel), st);
     }
     cudaMemsetAsync(overflow, 0, 4, st);
-    pack_kernel<<<(n_rows_sel + 3) / 4, 128, psmem, st>>>(a);
+    pack_kernel<<<std::max(1, n_rows_sel), 32 * kPackWarps, psmem, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return c.cuda_fail(e, "pack launch");
     int32_t ovf = 0;
