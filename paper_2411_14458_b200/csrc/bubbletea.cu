@@ -196,6 +196,7 @@ struct PackArgs {
   gpb_pack_summary* sums;
   gpb_placement* pl;        // nullable: [slot][req]
   int* overflow;
+  const int* order;         // CTA -> slot, most expensive first (nullable)
 };
 
 // A gap list: 16 bytes per gap (one load), x = start, y = end with the
@@ -596,7 +597,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 1) pack_kernel(PackArgs a) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   constexpr int BW = 32 * kPackWarps;  // requests per batch
-  const int si = blockIdx.x;
+  const int si = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   if (si >= a.n_slots) return;
   const TlSlot& sl = a.slots[si];
   const long long H = a.hz[si];
@@ -1366,7 +1367,7 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
   gpb_request* dreq = (gpb_request*)c.dev_buf(c.b_pl, sizeof(gpb_request) * std::max<int64_t>(1, n_req));
   gpb_pack_summary* dsum = (gpb_pack_summary*)c.dev_buf(c.b_sum, sizeof(gpb_pack_summary) * std::max(1, n_rows_sel) + 64);
   const long long G = gpu_base[n_rows_sel];
-  long long* gpu_arr = (long long*)c.dev_buf(c.b_pack_scratch, 16 * (size_t)std::max(1LL, G) + 8 * (n_rows_sel + 1));
+  long long* gpu_arr = (long long*)c.dev_buf(c.b_pack_scratch, 16 * (size_t)std::max(1LL, G) + 12 * (size_t)(n_rows_sel + 1));
   if (!dreq || !dsum || !gpu_arr) return c.cuda_fail(cudaErrorMemoryAllocation, "pack buffers");
   long long* gpu_off = gpu_arr;
   int* gpu_cnt = (int*)(gpu_off + std::max(1LL, G));
@@ -1384,6 +1385,23 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
   cudaMemcpyAsync(dsufmin, c.sufmin_host.data(), 8 * c.sufmin_host.size(), cudaMemcpyHostToDevice,
                   st);
   cudaMemcpyAsync(dbase, gpu_base.data(), 8 * n_rows_sel, cudaMemcpyHostToDevice, st);
+  // CTAs start in index order: the plans with the most searched stage GPUs
+  // (pipelines x stages searched one by one) first, so the longest packings
+  // do not start in the last wave
+  int32_t* dorder = (int32_t*)(dbase + n_rows_sel + 1);
+  c.pack_order.resize(n_rows_sel);
+  {
+    std::vector<long long> est(n_rows_sel);
+    for (int i = 0; i < n_rows_sel; ++i) {
+      const TlSlot& sl2 = slots[i];
+      const int d_eff = pm->inference_layers / sl2.D == 0 ? pm->inference_layers % sl2.D + 1 : sl2.D;
+      est[i] = (long long)sl2.C * sl2.S * d_eff;
+      c.pack_order[i] = i;
+    }
+    std::stable_sort(c.pack_order.begin(), c.pack_order.end(),
+                     [&](int x, int y) { return est[x] > est[y]; });
+  }
+  cudaMemcpyAsync(dorder, c.pack_order.data(), 4 * (size_t)n_rows_sel, cudaMemcpyHostToDevice, st);
   gpb_placement* dpl = nullptr;
   if (placements) {
     dpl = (gpb_placement*)c.dev_buf(c.b_placements, sizeof(gpb_placement) * (size_t)n_rows_sel * std::max<int64_t>(1, n_req));
@@ -1433,6 +1451,7 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
     a.sums = dsum;
     a.pl = dpl;
     a.overflow = overflow;
+    a.order = dorder;
     int max_pipes = 1;
     for (const TlSlot& sl2 : slots) max_pipes = std::max(max_pipes, sl2.C * sl2.S);
     a.max_pipes = max_pipes;

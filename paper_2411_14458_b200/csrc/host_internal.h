@@ -82,6 +82,7 @@ struct Ctx {
   std::vector<cudaEvent_t> side_done;
   Buf b_placements, b_ar;
   std::vector<long long> sufmin_host;  // pack: suffix-min arrivals (pinned by the call)
+  std::vector<int32_t> pack_order;     // pack: CTA -> slot launch order
   bool pack_allreduce = false;  // include the all-reduce tail in timelines
   // last build_timelines() outputs (device pointers into the buffers above)
   long long *tl_glo = nullptr, *tl_ghi = nullptr, *tl_gsum = nullptr, *tl_hz = nullptr;
