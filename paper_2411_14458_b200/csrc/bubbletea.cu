@@ -197,6 +197,7 @@ struct PackArgs {
   gpb_placement* pl;        // nullable: [slot][req]
   int* overflow;
   const int* order;         // CTA -> slot, most expensive first (nullable)
+  int order_base;           // first entry of `order` this launch covers
 };
 
 // A gap list: 16 bytes per gap (one load), x = start, y = end with the
@@ -583,21 +584,22 @@ __device__ __forceinline__ void group_caps(const PackArgs& a, const TlSlot& sl, 
   }
 }
 
-// One CTA of kPackWarps warps per plan runs the FCFS request loop
+// One CTA of W warps per plan runs the FCFS request loop
 // (schedule_prefills, bubbletea.cpp:132-222). Requests are staged 32 per warp
 // (one per lane: load, durations, arrival check) and searched speculatively
 // by every warp at once on the batch-start state (phase 1); warp 0 then
 // resolves the batch in FCFS order and commits (phase 2). A request is
 // examined only if it passes the plan-wide bound (some pipeline's caps admit
 // its durations).
-constexpr int kPackWarps = 4;
-
-__global__ void __launch_bounds__(32 * kPackWarps, 1) pack_kernel(PackArgs a) {
+// W = 4 for most plans (two CTAs per SM); the few most expensive plans get
+// W = 8 in a concurrent launch (they set the kernel's makespan).
+template <int W>
+__global__ void __launch_bounds__(32 * W, 1) pack_kernel(PackArgs a) {
   extern __shared__ __align__(16) long long pk_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  constexpr int BW = 32 * kPackWarps;  // requests per batch
-  const int si = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
+  constexpr int BW = 32 * W;  // requests per batch
+  const int si = a.order ? a.order[a.order_base + blockIdx.x] : (int)blockIdx.x;
   if (si >= a.n_slots) return;
   const TlSlot& sl = a.slots[si];
   const long long H = a.hz[si];
@@ -1391,7 +1393,7 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
   int32_t* dorder = (int32_t*)(dbase + n_rows_sel + 1);
   c.pack_order.resize(n_rows_sel);
   {
-    std::vector<long long> est(n_rows_sel);
+    std::vector<long long> est(std::max(1, n_rows_sel));
     for (int i = 0; i < n_rows_sel; ++i) {
       const TlSlot& sl2 = slots[i];
       const int d_eff = pm->inference_layers / sl2.D == 0 ? pm->inference_layers % sl2.D + 1 : sl2.D;
@@ -1400,6 +1402,7 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
     }
     std::stable_sort(c.pack_order.begin(), c.pack_order.end(),
                      [&](int x, int y) { return est[x] > est[y]; });
+    c.pack_est = est;
   }
   cudaMemcpyAsync(dorder, c.pack_order.data(), 4 * (size_t)n_rows_sel, cudaMemcpyHostToDevice, st);
   gpb_placement* dpl = nullptr;
@@ -1456,13 +1459,19 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
     for (const TlSlot& sl2 : slots) max_pipes = std::max(max_pipes, sl2.C * sl2.S);
     a.max_pipes = max_pipes;
     // caps, batch table, flags (pack_kernel's shared layout)
-    const size_t psmem = 16 * (size_t)max_pipes + (7 * 8 + 16 + 4 * 4) * (size_t)(32 * kPackWarps) +
-                         16 + 16 + (size_t)max_pipes + 16;
-    if (psmem > (size_t)c.smem_optin) {
+    auto psmem_of = [&](int W) {
+      return 16 * (size_t)max_pipes + (7 * 8 + 16 + 4 * 4) * (size_t)(32 * W) + 16 + 16 +
+             (size_t)max_pipes + 16;
+    };
+    const size_t psmem4 = psmem_of(4), psmem8 = psmem_of(8);
+    if (psmem8 > (size_t)c.smem_optin) {
       c.set_error("too many prefill pipelines per plan for the packing kernel");
       return GPB_CONFIG_ERROR;
     }
-    cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+    if (psmem4 > 48 * 1024)
+      cudaFuncSetAttribute(pack_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem4);
+    if (psmem8 > 48 * 1024)
+      cudaFuncSetAttribute(pack_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem8);
     a.memo_words = (pm->max_tokens + 31) / 32;
     const size_t memo_bytes = 4 * (size_t)a.memo_words * max_pipes * std::max(1, n_rows_sel);
     a.memo = (unsigned*)c.dev_buf(c.b_pack_memo, memo_bytes);
@@ -1474,7 +1483,30 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
       cudaMemsetAsync(a.stats, 0, 64 * (size_t)std::max(1, n_rows_sel), st);
     }
     cudaMemsetAsync(overflow, 0, 4, st);
-    pack_kernel<<<std::max(1, n_rows_sel), 32 * kPackWarps, psmem, st>>>(a);
+    // the heaviest plans (estimate within half of the largest, at most one
+    // per SM) on 8-warp CTAs on a side stream, the rest on 4-warp CTAs
+    int n_heavy = 0;
+    while (n_heavy < std::min(n_rows_sel, c.num_sms) &&
+           2 * c.pack_est[c.pack_order[n_heavy]] >= c.pack_est[c.pack_order[0]])
+      ++n_heavy;
+    if (n_heavy > 0) {
+      if (!c.pack_side) {
+        cudaStreamCreateWithFlags(&c.pack_side, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&c.pack_fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&c.pack_join, cudaEventDisableTiming);
+      }
+      cudaEventRecord(c.pack_fork, st);
+      cudaStreamWaitEvent(c.pack_side, c.pack_fork, 0);
+      PackArgs ah = a;
+      ah.order_base = 0;
+      pack_kernel<8><<<n_heavy, 32 * 8, psmem8, c.pack_side>>>(ah);
+      cudaEventRecord(c.pack_join, c.pack_side);
+    }
+    if (n_rows_sel - n_heavy > 0) {
+      a.order_base = n_heavy;
+      pack_kernel<4><<<n_rows_sel - n_heavy, 32 * 4, psmem4, st>>>(a);
+    }
+    if (n_heavy > 0) cudaStreamWaitEvent(st, c.pack_join, 0);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return c.cuda_fail(e, "pack launch");
     int32_t ovf = 0;

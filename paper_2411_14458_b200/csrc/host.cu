@@ -106,6 +106,9 @@ Ctx::~Ctx() {
     cudaEventDestroy(upload_ev);
   }
   if (stage) cudaFreeHost(stage);
+  if (pack_side) cudaStreamDestroy(pack_side);
+  if (pack_fork) cudaEventDestroy(pack_fork);
+  if (pack_join) cudaEventDestroy(pack_join);
   if (fork_ev) cudaEventDestroy(fork_ev);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);

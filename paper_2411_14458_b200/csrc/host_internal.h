@@ -83,6 +83,9 @@ struct Ctx {
   Buf b_placements, b_ar;
   std::vector<long long> sufmin_host;  // pack: suffix-min arrivals (pinned by the call)
   std::vector<int32_t> pack_order;     // pack: CTA -> slot launch order
+  std::vector<long long> pack_est;     // pack: per-slot cost estimate
+  cudaStream_t pack_side = nullptr;    // pack: the heavy plans' launch
+  cudaEvent_t pack_fork = nullptr, pack_join = nullptr;
   bool pack_allreduce = false;  // include the all-reduce tail in timelines
   // last build_timelines() outputs (device pointers into the buffers above)
   long long *tl_glo = nullptr, *tl_ghi = nullptr, *tl_gsum = nullptr, *tl_hz = nullptr;
