@@ -390,6 +390,8 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   }
   std::vector<int32_t> work;
   work.reserve(n_rows);
+  std::vector<int32_t> bscen;
+  bscen.reserve(n_scen);
   for (auto& [key, list] : by_key) {
     std::stable_sort(list.begin(), list.end(), [&](int a, int b) { return cost(a) > cost(b); });
     Bucket b;
@@ -410,6 +412,9 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
       b.max_nw = std::max(b.max_nw, ds[i].n_order - 1);
     }
     b.count = (int32_t)work.size() - b.offset;
+    b.scen_off = (int32_t)bscen.size();
+    b.scen_cnt = (int32_t)list.size();
+    for (int i : list) bscen.push_back(i);
     b.cost = cost(list.front());
     // makespan estimate: the longest row, or the whole bucket spread over
     // ~8 resident warps per SM
@@ -421,14 +426,21 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   std::stable_sort(c.buckets.begin(), c.buckets.end(), [&](const Bucket& x, const Bucket& y) {
     return rank(x) != rank(y) ? rank(x) < rank(y) : x.cost > y.cost;
   });
+  c.sel_blocks = 0;
+  for (Bucket& b : c.buckets) {
+    b.sel_grid = b.count > 0 ? std::max(1, std::min(256, (b.scen_cnt + 3) / 4)) : 0;
+    b.sel_off = c.sel_blocks;
+    c.sel_blocks += b.sel_grid;
+  }
 
   // Upload: the tables are staged in one pinned buffer and copied
   // asynchronously on the launch stream (evaluate is ordered after them).
   cudaStream_t st = c.stream;
   const size_t sz_t = sizeof(DevTopo) * dt.size(), sz_s = sizeof(DevScen) * ds.size(),
-               sz_r = sizeof(int32_t) * row_scen.size(), sz_w = sizeof(int32_t) * work.size();
+               sz_r = sizeof(int32_t) * row_scen.size(), sz_w = sizeof(int32_t) * work.size(),
+               sz_b = sizeof(int32_t) * bscen.size();
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  const size_t stage_need = al(sz_t) + al(sz_s) + al(sz_r) + al(sz_w);
+  const size_t stage_need = al(sz_t) + al(sz_s) + al(sz_r) + al(sz_w) + al(sz_b);
   if (c.upload_pending) {  // the previous upload must have left the staging buffer
     cudaEventSynchronize(c.upload_ev);
     c.upload_pending = false;
@@ -455,10 +467,11 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   };
   if (!up(c.b_topos, dt.data(), sz_t) || !up(c.b_scens, ds.data(), sz_s) ||
       !up(c.b_row_scen, row_scen.data(), sz_r) || !up(c.b_work, work.data(), sz_w) ||
+      !up(c.b_bscen, bscen.data(), sz_b) ||
       !c.dev_buf(c.b_rows, sizeof(gpb_row) * std::max<int64_t>(n_rows, 1)) ||
       !c.dev_buf(c.b_results, sizeof(gpb_scenario_result) * std::max(n_scen, 1)) ||
       !c.dev_buf(c.b_cursors, sizeof(int32_t) * (c.buckets.size() + 1)) ||
-      !c.dev_buf(c.b_best, sizeof(gpb_best) * 1024)) {
+      !c.dev_buf(c.b_best, sizeof(gpb_best) * (2 + (size_t)c.sel_blocks))) {
     return c.cuda_fail(cudaGetLastError(), "upload");
   }
   cudaEventRecord(c.upload_ev, st);
@@ -545,23 +558,28 @@ static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
     if (e != cudaSuccess) return c.cuda_fail(e, "eval launch");
     if (bt) rec(c.bucket_ev_end[bi], ss);
     ++launches;
+    // select() over the bucket's scenarios (dc_select.cpp:99-123), on its stream
+    SelectArgs sa;
+    sa.scens = (const DevScen*)c.b_scens.ptr;
+    sa.scen_list = (const int32_t*)c.b_bscen.ptr + b.scen_off;
+    sa.n_scen = b.scen_cnt;
+    sa.rows = (gpb_row*)c.b_rows.ptr;
+    sa.results = (gpb_scenario_result*)c.b_results.ptr;
+    sa.block_best = (gpb_best*)c.b_best.ptr + 1 + b.sel_off;
+    sa.best = (gpb_best*)c.b_best.ptr;
+    if ((e = launch_select_part(sa, b.sel_grid, ss)) != cudaSuccess)
+      return c.cuda_fail(e, "select launch");
+    ++launches;
   }
   for (size_t k = 0; k < n_side; ++k) {  // join
     cudaEventRecord(c.side_done[k], c.side[k]);
     cudaStreamWaitEvent(st, c.side_done[k], 0);
   }
   rec(c.ev1, st);
-  SelectArgs sa;
-  sa.scens = (const DevScen*)c.b_scens.ptr;
-  sa.n_scen = c.n_scen;
-  sa.rows = (gpb_row*)c.b_rows.ptr;
-  sa.results = (gpb_scenario_result*)c.b_results.ptr;
-  sa.block_best = (gpb_best*)c.b_best.ptr + 1;
-  sa.best = (gpb_best*)c.b_best.ptr;
-  const int sgrid = std::max(1, std::min(1023, (c.n_scen + 3) / 4));
-  cudaError_t e = launch_select(sa, sgrid, st);
+  cudaError_t e = launch_best_reduce((gpb_best*)c.b_best.ptr + 1, c.sel_blocks,
+                                     (gpb_best*)c.b_best.ptr, st);
   if (e != cudaSuccess) return c.cuda_fail(e, "select launch");
-  launches += 2;
+  launches += 1;
   rec(c.ev2, st);
   c.last_launches = launches + 1;  // + the cursor memset
   return GPB_OK;

@@ -36,6 +36,10 @@ struct Bucket {
   double cost = 0;  // estimated cost of the bucket's heaviest row
   int stream = 0;   // side stream it ran on
   bool heavy = false;  // ATLAS rows near the heaviest estimate (launched first)
+  // its scenarios (every row of a scenario lands in one bucket): selected on
+  // the bucket's stream as soon as its kernel ends
+  int32_t scen_off = 0, scen_cnt = 0;
+  int32_t sel_grid = 0, sel_off = 0;  // select blocks and their block_best slots
 };
 
 // Launch shape of one ATLAS kernel (evaluation or timeline variant) over
@@ -69,7 +73,8 @@ struct Ctx {
   std::vector<int32_t> work_host;  // bucket work lists (profiling)
 
   // device tables
-  Buf b_topos, b_scens, b_row_scen, b_work, b_rows, b_results, b_cursors, b_best;
+  Buf b_topos, b_scens, b_row_scen, b_work, b_rows, b_results, b_cursors, b_best, b_bscen;
+  int32_t sel_blocks = 0;  // select blocks over all buckets
   Buf b_scratch, b_cycles;
   bool profile_rows = false;
   // timeline / bubbletea buffers
@@ -115,7 +120,7 @@ struct Ctx {
   bool upload_pending = false;
 
   std::vector<Buf*> all_bufs() {
-    return {&b_topos, &b_scens, &b_row_scen, &b_work, &b_rows, &b_results, &b_cursors,
+    return {&b_topos, &b_scens, &b_row_scen, &b_work, &b_bscen, &b_rows, &b_results, &b_cursors,
             &b_best, &b_scratch, &b_cycles, &b_tl_rows, &b_tl_spans, &b_tl_nspan, &b_tl_scratch,
             &b_gaps, &b_ngaps, &b_reqs, &b_pl, &b_sum, &b_pack_scratch, &b_pack_misc, &b_sufmin, &b_pack_stats, &b_pack_memo,
             &b_placements, &b_ar};

@@ -43,6 +43,7 @@ struct EvalArgs {
 
 struct SelectArgs {
   const DevScen* scens;
+  const int32_t* scen_list;   // scenarios to select (nullable: 0 .. n_scen-1)
   int32_t n_scen;
   gpb_row* rows;
   gpb_scenario_result* results;
@@ -55,6 +56,9 @@ cudaError_t launch_onef1b(int B, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_atlas(int B, const EvalArgs& a, int grid, int wpc, cudaStream_t st);
 int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem);
 cudaError_t launch_select(const SelectArgs& a, int grid, cudaStream_t st);
+// select_kernel alone (per bucket) / the final reduction of the block bests
+cudaError_t launch_select_part(const SelectArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_best_reduce(const gpb_best* in, int n, gpb_best* out, cudaStream_t st);
 cudaError_t launch_timeline(int policy, int B, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_atlas_timeline(int B, const EvalArgs& a, int grid, int wpc, cudaStream_t st);
 

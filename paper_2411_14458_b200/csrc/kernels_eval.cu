@@ -331,8 +331,9 @@ __global__ void __launch_bounds__(kEvalThreads) select_kernel(SelectArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double best_thr = -1.0;
   long long best_row = -1;
-  for (int si = blockIdx.x * (blockDim.x >> 5) + warp; si < a.n_scen;
-       si += gridDim.x * (blockDim.x >> 5)) {
+  for (int wi = blockIdx.x * (blockDim.x >> 5) + warp; wi < a.n_scen;
+       wi += gridDim.x * (blockDim.x >> 5)) {
+    const int si = a.scen_list ? a.scen_list[wi] : wi;
     const DevScen& sc = a.scens[si];
     // chunked scan: lane-local first max, then ordered warp combine
     double cthr = -1.0;
@@ -468,6 +469,16 @@ cudaError_t launch_onef1b(int B, const EvalArgs& a, int grid, cudaStream_t st) {
 cudaError_t launch_select(const SelectArgs& a, int grid, cudaStream_t st) {
   select_kernel<<<grid, kEvalThreads, 0, st>>>(a);
   best_reduce_kernel<<<1, 32, 0, st>>>(a.block_best, grid, a.best);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_part(const SelectArgs& a, int grid, cudaStream_t st) {
+  select_kernel<<<grid, kEvalThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_best_reduce(const gpb_best* in, int n, gpb_best* out, cudaStream_t st) {
+  best_reduce_kernel<<<1, 32, 0, st>>>(in, n, out);
   return cudaGetLastError();
 }
 
