@@ -124,20 +124,19 @@ Ctx::~Ctx() {
 // ------------------------------------------------------------ validation
 
 static void validate_topology(const gpb_topology& t, int idx) {
-  char p[64];
-  snprintf(p, sizeof p, "topologies[%d]", idx);
+  const auto p = [idx] { return "topologies[" + std::to_string(idx) + "]"; };  // errors only
   if (t.n_dc < 1 || t.n_dc > GPB_MAX_DC)
-    throw ConfigErr{std::string(p) + ".n_dc: must be in [1, 8]"};
+    throw ConfigErr{p() + ".n_dc: must be in [1, 8]"};
   for (int i = 0; i < t.n_dc; ++i) {
-    if (t.gpu_count[i] < 0) throw ConfigErr{std::string(p) + ".gpu_count: must be >= 0"};
-    if (!(t.intra_bw[i] > 0)) throw ConfigErr{std::string(p) + ".intra_bw: must be > 0"};
+    if (t.gpu_count[i] < 0) throw ConfigErr{p() + ".gpu_count: must be >= 0"};
+    if (!(t.intra_bw[i] > 0)) throw ConfigErr{p() + ".intra_bw: must be > 0"};
     for (int j = 0; j < t.n_dc; ++j)
       if (!(t.latency_ms[i][j] >= 0))
-        throw ConfigErr{std::string(p) + ".latency_ms: must be >= 0"};
+        throw ConfigErr{p() + ".latency_ms: must be >= 0"};
   }
-  if (!(t.pair_bw_cap > 0)) throw ConfigErr{std::string(p) + ".pair_bw_cap: must be > 0"};
+  if (!(t.pair_bw_cap > 0)) throw ConfigErr{p() + ".pair_bw_cap: must be > 0"};
   if (t.n_tcp < 0 || t.n_tcp > GPB_MAX_TCP)
-    throw ConfigErr{std::string(p) + ".n_tcp: must be in [0, 8]"};
+    throw ConfigErr{p() + ".n_tcp: must be in [0, 8]"};
   for (int i = 0; i < t.n_tcp; ++i) {  // validate_tcp_table (topology.cpp:56-76)
     if (t.tcp_latency_ms[i] <= 0 || t.tcp_bw[i] <= 0)
       throw ConfigErr{"wan.tcp_table: latency and bandwidth must be positive"};
@@ -156,10 +155,8 @@ static int64_t act_bytes(const gpb_scenario& s) {
 
 static void validate_scenario(const gpb_scenario& s, int idx, int n_topo,
                               const gpb_topology* topos) {
-  char p[64];
-  snprintf(p, sizeof p, "scenarios[%d]", idx);
-  const std::string P(p);
-  if (s.topology < 0 || s.topology >= n_topo) throw ConfigErr{P + ".topology: out of range"};
+  const auto P = [idx] { return P_(idx); };  // built only for an error message
+  if (s.topology < 0 || s.topology >= n_topo) throw ConfigErr{P() + ".topology: out of range"};
   const gpb_topology& t = topos[s.topology];
   if (s.policy < 0 || s.policy > 3)
     throw ConfigErr{"policy: must be one of gpipe, 1f1b, varuna, atlas"};
@@ -169,7 +166,7 @@ static void validate_scenario(const gpb_scenario& s, int idx, int n_topo,
   if (s.layers_per_partition < 1) throw ConfigErr{"model.layers_per_partition: must be >= 1"};
   if (s.num_microbatches < 1) throw ConfigErr{"model.num_microbatches: must be >= 1"};
   if (s.num_microbatches > 65535)
-    throw ConfigErr{P + ": more than 65535 microbatches is outside the kernel envelope"};
+    throw ConfigErr{P() + ": more than 65535 microbatches is outside the kernel envelope"};
   if (s.bytes_per_element < 1 || s.hidden < 1 || s.seq_len < 1 || s.microbatch < 1)
     throw ConfigErr{"model: dimensions must be >= 1"};
   if (s.params_per_layer < 0) throw ConfigErr{"model.params_per_layer: must be >= 0"};
@@ -180,13 +177,13 @@ static void validate_scenario(const gpb_scenario& s, int idx, int n_topo,
     throw ConfigErr{"compute: durations must be positive"};  // workload.cpp:11-13
   }
   if (s.d_max < 0) throw ConfigErr{"select.d_max: must be >= 1"};
-  if (s.n_order < 0 || s.n_order > t.n_dc) throw ConfigErr{P + ".n_order: out of range"};
+  if (s.n_order < 0 || s.n_order > t.n_dc) throw ConfigErr{P() + ".n_order: out of range"};
   unsigned seen = 0;
   for (int i = 0; i < s.n_order; ++i) {
     const int dc = s.dc_order[i];
     if (dc < 0 || dc >= t.n_dc) throw ConfigErr{"datacenters: unknown datacenter id"};
     if (seen & (1u << dc))
-      throw ConfigErr{P + ".dc_order: duplicate datacenter (unsupported, see DESIGN.md)"};
+      throw ConfigErr{P() + ".dc_order: duplicate datacenter (unsupported, see DESIGN.md)"};
     seen |= 1u << dc;
   }
   if (s.mem_limit < 0) throw ConfigErr{"mem_limit: must be >= 1"};
@@ -194,7 +191,7 @@ static void validate_scenario(const gpb_scenario& s, int idx, int n_topo,
     throw ConfigErr{"simulate.n_connections: must be >= 1"};
   const int S = (s.num_layers + s.layers_per_partition - 1) / s.layers_per_partition;
   if (S > 256)
-    throw ConfigErr{P + ": more than 256 pipeline stages is outside the kernel envelope"};
+    throw ConfigErr{P() + ": more than 256 pipeline stages is outside the kernel envelope"};
   if (act_bytes(s) <= 0) throw ConfigErr{"model: activation size overflow"};
 }
 
