@@ -227,6 +227,15 @@ const char* gpb_last_error(gpb_ctx* ctx) {
   return ctx ? reinterpret_cast<Ctx*>(ctx)->last_error.c_str() : "";
 }
 
+// GPB_NO_GROUP_FLUSH=1: one warp per flush row (A/B switch)
+static const bool kNoGroupFlush = std::getenv("GPB_NO_GROUP_FLUSH") != nullptr;
+// spaces with fewer rows keep one warp per flush row (GPB_GROUP_FLUSH_MIN_ROWS
+// overrides, read at every load: tests force the grouped kernel)
+static int64_t group_flush_min_rows() {
+  const char* e = std::getenv("GPB_GROUP_FLUSH_MIN_ROWS");
+  return e ? std::atoll(e) : 200000;
+}
+
 static bool same_shapes(const std::vector<Bucket>& a, const std::vector<Bucket>& b) {
   if (a.size() != b.size()) return false;
   for (size_t i = 0; i < a.size(); ++i) {
@@ -234,7 +243,7 @@ static bool same_shapes(const std::vector<Bucket>& a, const std::vector<Bucket>&
     if (x.policy != y.policy || x.B != y.B || x.offset != y.offset || x.count != y.count ||
         x.max_m != y.max_m || x.max_cs != y.max_cs || x.max_cm != y.max_cm ||
         x.max_csm != y.max_csm || x.max_c != y.max_c || x.max_s != y.max_s ||
-        x.max_nw != y.max_nw || x.heavy != y.heavy)
+        x.max_nw != y.max_nw || x.heavy != y.heavy || x.gw != y.gw)
       return false;
   }
   return true;
@@ -380,10 +389,23 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   double max_atlas = 0;
   for (int i = 0; i < n_scen; ++i)
     if (ds[i].policy == GPB_ATLAS) max_atlas = std::max(max_atlas, cost(i));
-  std::map<std::tuple<int, int, int>, std::vector<int>> by_key;
+  // in large (throughput-bound) spaces, flush rows of shallow pipelines
+  // (S <= 8 / 16) get their own buckets with several rows per warp
+  // (flush_group_kernel); small spaces are bound by their longest row and
+  // keep fewer buckets (measured: config 2 0.59 -> 0.63 ms with the split,
+  // config 5 387 -> 369 ms)
+  const int64_t group_min = group_flush_min_rows();
+  auto gw_of = [&](const DevScen& d) {
+    if ((d.policy != GPB_GPIPE && d.policy != GPB_VARUNA) || kNoGroupFlush || n_rows < group_min)
+      return 32;
+    const int gw = d.S <= 8 ? 8 : (d.S <= 16 ? 16 : 32);
+    // the per-row last-stage buffer (M entries per row) must fit the block
+    return (size_t)(kEvalThreads / gw) * d.M * 8 <= 160 * 1024 ? gw : 32;
+  };
+  std::map<std::tuple<int, int, int, int>, std::vector<int>> by_key;
   for (int i = 0; i < n_scen; ++i) {
     const int heavy = ds[i].policy == GPB_ATLAS && cost(i) >= 0.3 * max_atlas;
-    by_key[{ds[i].policy, (ds[i].S + 31) / 32, heavy}].push_back(i);
+    by_key[{ds[i].policy, (ds[i].S + 31) / 32, heavy, gw_of(ds[i])}].push_back(i);
   }
   std::vector<int32_t> work;
   work.reserve(n_rows);
@@ -395,6 +417,7 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
     b.policy = std::get<0>(key);
     b.B = std::get<1>(key);
     b.heavy = std::get<2>(key) != 0;
+    b.gw = std::get<3>(key);
     b.offset = (int32_t)work.size();
     double total = 0;
     for (int i : list) {
@@ -541,7 +564,10 @@ static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
     cudaError_t e;
     if (b.policy == GPB_GPIPE || b.policy == GPB_VARUNA) {
       a.smem_m = b.max_m;
-      e = launch_flush(b.B, b.policy == GPB_GPIPE, a, grid, ss);
+      e = b.gw < 32 ? launch_flush_group(b.gw, b.policy == GPB_GPIPE, a,
+                                         std::min(grid_eval, (b.count + 4 * (32 / b.gw) - 1) /
+                                                                 (4 * (32 / b.gw))), ss)
+                    : launch_flush(b.B, b.policy == GPB_GPIPE, a, grid, ss);
     } else if (b.policy == GPB_1F1B) {
       e = launch_onef1b(b.B, a, grid, ss);
     } else {

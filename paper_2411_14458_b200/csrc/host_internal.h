@@ -36,6 +36,7 @@ struct Bucket {
   double cost = 0;  // estimated cost of the bucket's heaviest row
   int stream = 0;   // side stream it ran on
   bool heavy = false;  // ATLAS rows near the heaviest estimate (launched first)
+  int gw = 32;         // flush rows per warp = 32 / gw (flush_group_kernel when < 32)
   // its scenarios (every row of a scenario lands in one bucket): selected on
   // the bucket's stream as soon as its kernel ends
   int32_t scen_off = 0, scen_cnt = 0;

@@ -52,6 +52,8 @@ struct SelectArgs {
 };
 
 cudaError_t launch_flush(int B, bool gpipe, const EvalArgs& a, int grid, cudaStream_t st);
+// shallow pipelines (S <= gw, gw = 8 or 16): 32/gw rows per warp
+cudaError_t launch_flush_group(int gw, bool gpipe, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_onef1b(int B, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_atlas(int B, const EvalArgs& a, int grid, int wpc, cudaStream_t st);
 int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem);

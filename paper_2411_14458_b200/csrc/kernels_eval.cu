@@ -122,6 +122,112 @@ __global__ void __launch_bounds__(kEvalThreads) flush_kernel(EvalArgs a) {
   }
 }
 
+// Shallow pipelines (S <= GW <= 16): 32/GW rows per warp, one group of GW
+// lanes per row (lane = stage), the same wavefronts as flush_row with
+// segmented shuffles. The loop bounds are the warp's maximum so every lane
+// reaches every shuffle; a group past its own row's range idles.
+template <bool GPIPE, int GW>
+__global__ void __launch_bounds__(kEvalThreads) flush_group_kernel(EvalArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int NG = 32 / GW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gi = lane / GW, s = lane % GW;  // group in the warp, stage in the row
+  long long* fdl = reinterpret_cast<long long*>(smem) + ((size_t)warp * NG + gi) * a.smem_m;
+  for (;;) {
+    int w0 = 0;
+    if (lane == 0) w0 = atomicAdd(a.cursor, NG);
+    w0 = __shfl_sync(kFull, w0, 0);
+    if (w0 >= a.n_work) break;
+    const int wk = w0 + gi;
+    const long long t_start = clock64();
+    bool ok = false;
+    int row = 0, si = 0;
+    Geom g;
+    if (wk < a.n_work) {
+      row = a.work[wk];
+      si = a.row_scen[row];
+      const DevScen& sc = a.scens[si];
+      const int d = (int)(row - sc.first_row) + 1;
+      decode(sc, a.topos[sc.topo], d, g);
+      ok = g.feasible;
+      if (!ok && s == 0) {
+        gpb_row r;
+        infeasible_row(r);
+        r.scenario = si;
+        r.d = d;
+        a.rows[row] = r;
+      }
+    }
+    const int S = ok ? g.S : 0, M = ok ? g.M : 0;
+    const int K = S > 0 ? S - 1 : 0;  // the group's last stage lane
+    int T = ok ? M + K : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) T = max(T, __shfl_xor_sync(kFull, T, o));
+    StageLinks<1> L;
+    if (ok) L.load(g, s, false);
+    long long gf = 0, lf = 0, lb = 0;
+    const long long fwd = ok ? g.fwd : 0, dur = ok ? g.dur : 0;
+    // forward: E[s][m] = max(A[s][m], E[s][m-1]) + f; link FIFO per boundary
+    long long a_in = 0;
+    for (int t = 0; t < T; ++t) {
+      const int m = t - s;
+      long long av = s == 0 ? 0 : a_in;
+      if (ok && s <= K && m >= 0 && m < M) {
+        const long long e = imax(av, gf) + fwd;
+        gf = e;
+        if (s == S - 1) fdl[m] = e;
+        if (L.wanf & 1u) {
+          const long long occ = imax(e, lf) + L.serf[0];
+          lf = occ;
+          av = occ + L.latf[0];
+        } else {
+          av = e;
+        }
+      }
+      a_in = __shfl_up_sync(kFull, av, 1, GW);
+    }
+    __syncwarp();
+    const long long beta = GPIPE && ok ? fdl[M - 1] : 0;  // barrier_last_fwd
+    // drain: stages S-1..0, microbatch order k (varuna) or M-1-k (gpipe)
+    long long g_in = 0;
+    for (int t = 0; t < T; ++t) {
+      const int i = t - (K - s);
+      long long gv = g_in;
+      if (ok && s <= K && i >= 0 && i < M) {
+        const int m = GPIPE ? M - 1 - i : i;
+        long long ready = s == S - 1 ? fdl[m] : gv;
+        ready = imax(ready, beta);
+        const long long z = imax(ready, gf) + dur;
+        gf = z;
+        if (s > 0) {
+          if (L.wanb & 1u) {
+            const long long occ = imax(z, lb) + L.serb[0];
+            lb = occ;
+            gv = occ + L.latb[0];
+          } else {
+            gv = z;
+          }
+        }
+      }
+      g_in = __shfl_down_sync(kFull, gv, 1, GW);
+    }
+    long long mk = ok && s < S ? gf : 0;
+#pragma unroll
+    for (int o = GW / 2; o > 0; o >>= 1) mk = imax(mk, __shfl_xor_sync(kFull, mk, o, GW));
+    if (ok && s == 0) {
+      const DevScen& sc = a.scens[si];
+      if (a.row_cycles) a.row_cycles[row] = clock64() - t_start;
+      gpb_row r;
+      infeasible_row(r);
+      r.scenario = si;
+      r.d = g.D;
+      finish_row(sc, a.topos[sc.topo], g, mk, r);
+      a.rows[row] = r;
+    }
+    __syncwarp();
+  }
+}
+
 // ----------------------------------------------------------------- 1F1B
 
 // Item at program counter pc of stage s (w = min(S - s, M) warm-up forwards,
@@ -433,6 +539,36 @@ static cudaError_t launch_flush_b(bool gpipe, const EvalArgs& a, int grid, cudaS
       cudaFuncSetAttribute(flush_kernel<B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
     flush_kernel<B, false><<<grid, kEvalThreads, smem, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flush_group(int gw, bool gpipe, const EvalArgs& a, int grid, cudaStream_t st) {
+  const size_t smem = (size_t)(kEvalThreads / gw) * a.smem_m * sizeof(long long);
+  if (gw == 8) {
+    if (gpipe) {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(flush_group_kernel<true, 8>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      flush_group_kernel<true, 8><<<grid, kEvalThreads, smem, st>>>(a);
+    } else {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(flush_group_kernel<false, 8>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      flush_group_kernel<false, 8><<<grid, kEvalThreads, smem, st>>>(a);
+    }
+  } else {
+    if (gpipe) {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(flush_group_kernel<true, 16>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      flush_group_kernel<true, 16><<<grid, kEvalThreads, smem, st>>>(a);
+    } else {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(flush_group_kernel<false, 16>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      flush_group_kernel<false, 16><<<grid, kEvalThreads, smem, st>>>(a);
+    }
   }
   return cudaGetLastError();
 }
