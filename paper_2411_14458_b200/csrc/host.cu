@@ -389,15 +389,14 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   double max_atlas = 0;
   for (int i = 0; i < n_scen; ++i)
     if (ds[i].policy == GPB_ATLAS) max_atlas = std::max(max_atlas, cost(i));
-  // in large (throughput-bound) spaces, flush rows of shallow pipelines
-  // (S <= 8 / 16) get their own buckets with several rows per warp
-  // (flush_group_kernel); small spaces are bound by their longest row and
+  // in large (throughput-bound) spaces, gpipe/varuna/1f1b rows of shallow
+  // pipelines (S <= 8 / 16) get their own buckets with several rows per warp
+  // (flush_group_kernel, onef1b_group_kernel); small spaces are bound by their longest row and
   // keep fewer buckets (measured: config 2 0.59 -> 0.63 ms with the split,
   // config 5 387 -> 369 ms)
   const int64_t group_min = group_flush_min_rows();
   auto gw_of = [&](const DevScen& d) {
-    if ((d.policy != GPB_GPIPE && d.policy != GPB_VARUNA) || kNoGroupFlush || n_rows < group_min)
-      return 32;
+    if (d.policy == GPB_ATLAS || kNoGroupFlush || n_rows < group_min) return 32;
     const int gw = d.S <= 8 ? 8 : (d.S <= 16 ? 16 : 32);
     // the per-row last-stage buffer (M entries per row) must fit the block
     return (size_t)(kEvalThreads / gw) * d.M * 8 <= 160 * 1024 ? gw : 32;
@@ -569,7 +568,10 @@ static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
                                                                  (4 * (32 / b.gw))), ss)
                     : launch_flush(b.B, b.policy == GPB_GPIPE, a, grid, ss);
     } else if (b.policy == GPB_1F1B) {
-      e = launch_onef1b(b.B, a, grid, ss);
+      e = b.gw < 32 ? launch_onef1b_group(b.gw, a,
+                                          std::min(grid_eval, (b.count + 4 * (32 / b.gw) - 1) /
+                                                                  (4 * (32 / b.gw))), ss)
+                    : launch_onef1b(b.B, a, grid, ss);
     } else {
       const AtlasPlan& P = c.aplan[bi];
       a.lay = P.L;

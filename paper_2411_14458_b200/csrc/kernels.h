@@ -55,6 +55,7 @@ cudaError_t launch_flush(int B, bool gpipe, const EvalArgs& a, int grid, cudaStr
 // shallow pipelines (S <= gw, gw = 8 or 16): 32/gw rows per warp
 cudaError_t launch_flush_group(int gw, bool gpipe, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_onef1b(int B, const EvalArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_onef1b_group(int gw, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_atlas(int B, const EvalArgs& a, int grid, int wpc, cudaStream_t st);
 int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem);
 cudaError_t launch_select(const SelectArgs& a, int grid, cudaStream_t st);

@@ -346,6 +346,126 @@ __device__ long long onef1b_row(const Geom& g, int& err, long long* tfe = nullpt
   return warp_max64(mk);
 }
 
+// Shallow 1F1B pipelines (S <= GW <= 16): 32/GW rows per warp, one group of
+// GW lanes per row (lane = stage), onef1b_row's lock-step rounds with
+// segmented shuffles; the round loop runs while any row of the warp is busy.
+template <int GW>
+__global__ void __launch_bounds__(kEvalThreads) onef1b_group_kernel(EvalArgs a) {
+  constexpr int NG = 32 / GW;
+  const int lane = threadIdx.x & 31;
+  const int gi = lane / GW, s = lane % GW;
+  for (;;) {
+    int w0 = 0;
+    if (lane == 0) w0 = atomicAdd(a.cursor, NG);
+    w0 = __shfl_sync(kFull, w0, 0);
+    if (w0 >= a.n_work) break;
+    const int wk = w0 + gi;
+    const long long t_start = clock64();
+    bool ok = false;
+    int row = 0, si = 0;
+    Geom g;
+    if (wk < a.n_work) {
+      row = a.work[wk];
+      si = a.row_scen[row];
+      const DevScen& sc = a.scens[si];
+      const int d = (int)(row - sc.first_row) + 1;
+      decode(sc, a.topos[sc.topo], d, g);
+      ok = g.feasible;
+      if (!ok && s == 0) {
+        gpb_row r;
+        infeasible_row(r);
+        r.scenario = si;
+        r.d = d;
+        a.rows[row] = r;
+      }
+    }
+    const int S = ok ? g.S : 0, M = ok ? g.M : 0;
+    StageLinks<1> L;
+    if (ok) L.load(g, s, false);
+    int pc = ok && s < S ? 0 : 2 * M, nF = 0, nB = 0;
+    long long gf = 0, lf = 0, lb = 0, outF = 0, outB = 0, fdo = 0;
+    int bad = 0;
+    for (;;) {
+      if (!__any_sync(kFull, pc < 2 * M)) break;
+      // snapshots of the neighbours' state at the start of the round
+      const int lnF = __shfl_up_sync(kFull, nF, 1, GW);
+      const long long loutF = __shfl_up_sync(kFull, outF, 1, GW);
+      const int rnB = __shfl_down_sync(kFull, nB, 1, GW);
+      const long long routB = __shfl_down_sync(kFull, outB, 1, GW);
+      if (pc >= 2 * M) continue;
+      const int w = min(S - s, M);
+      bool fwd;
+      int m;
+      onef1b_item(pc, w, M, fwd, m);
+      if (fwd) {
+        long long arr = 0;
+        if (s > 0) {
+          if (lnF <= m) continue;           // input not produced yet
+          if (lnF > m + 1) bad = 1;         // mailbox depth invariant
+          arr = loutF;
+        }
+        const long long e = imax(arr, gf) + g.fwd;
+        gf = e;
+        fdo = e;
+        if (s + 1 < S) {
+          if (L.wanf & 1u) {
+            const long long occ = imax(e, lf) + L.serf[0];
+            lf = occ;
+            outF = occ + L.latf[0];
+          } else {
+            outF = e;
+          }
+        }
+        nF += 1;
+      } else {
+        long long ready;
+        if (s == S - 1) {
+          if (nF <= m) continue;
+          ready = fdo;  // F(S-1, m) immediately precedes B(S-1, m)
+        } else {
+          if (rnB <= m) continue;
+          if (rnB > m + 1) bad = 1;
+          ready = routB;
+        }
+        const long long z = imax(ready, gf) + g.dur;
+        gf = z;
+        if (s > 0) {
+          if (L.wanb & 1u) {
+            const long long occ = imax(z, lb) + L.serb[0];
+            lb = occ;
+            outB = occ + L.latb[0];
+          } else {
+            outB = z;
+          }
+        }
+        nB += 1;
+      }
+      pc += 1;
+    }
+    long long mk = ok && s < S ? gf : 0;
+#pragma unroll
+    for (int o = GW / 2; o > 0; o >>= 1) {
+      mk = imax(mk, __shfl_xor_sync(kFull, mk, o, GW));
+      bad |= __shfl_xor_sync(kFull, bad, o, GW);
+    }
+    if (ok && s == 0) {
+      const DevScen& sc = a.scens[si];
+      if (a.row_cycles) a.row_cycles[row] = clock64() - t_start;
+      gpb_row r;
+      infeasible_row(r);
+      r.scenario = si;
+      r.d = g.D;
+      finish_row(sc, a.topos[sc.topo], g, mk, r);
+      if (bad) {
+        r.feasible = -1;  // kernel-side invariant failure: host raises GPB_ERROR
+        atomicExch(a.error_flag, 1);
+      }
+      a.rows[row] = r;
+    }
+    __syncwarp();
+  }
+}
+
 template <int B>
 __global__ void __launch_bounds__(kEvalThreads) onef1b_kernel(EvalArgs a) {
   for (;;) {
@@ -585,6 +705,14 @@ cudaError_t launch_flush(int B, bool gpipe, const EvalArgs& a, int grid, cudaStr
     case 8: return launch_flush_b<8>(gpipe, a, grid, st);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_onef1b_group(int gw, const EvalArgs& a, int grid, cudaStream_t st) {
+  if (gw == 8)
+    onef1b_group_kernel<8><<<grid, kEvalThreads, 0, st>>>(a);
+  else
+    onef1b_group_kernel<16><<<grid, kEvalThreads, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_onef1b(int B, const EvalArgs& a, int grid, cudaStream_t st) {
