@@ -1059,8 +1059,16 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
   return warp_max64(mk);
 }
 
+// Blocks per SM the register allocation must allow: 3 for one stage per lane
+// (162 registers, no spills: more resident warps when the space saturates
+// the GPU), 1 for deeper pipelines (their larger per-lane state would spill).
+#ifndef GPB_ATLAS_MIN_BLOCKS_B1
+#define GPB_ATLAS_MIN_BLOCKS_B1 3
+#endif
+
 template <int B>
-__global__ void __launch_bounds__(kEvalThreads, 1) atlas_kernel(EvalArgs a) {
+__global__ void __launch_bounds__(kEvalThreads, B == 1 ? GPB_ATLAS_MIN_BLOCKS_B1 : 1)
+    atlas_kernel(EvalArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
