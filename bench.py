@@ -123,8 +123,8 @@ def impl_reference(args):
     topos, scens = workloads.config2(args.rows, seed=1)
     idx, n_rows = cpu_sample(topos, scens)
     threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        pass  # the reference has no warm-up state; steps are independent
+    for _ in range(args.warmup):  # untimed (page cache, allocator, thread pool)
+        run_cpu(topos, scens, idx, threads)
     times = []
     kind = "reference"
     for _ in range(args.steps):
