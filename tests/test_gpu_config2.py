@@ -42,3 +42,47 @@ def test_config2_all_rows_bit_exact(planner, checker):
                 best = (b.throughput, r0 + k)
     got = planner.best()
     assert (got.throughput, got.row) == best
+
+
+def test_two_sessions_pipelined(planner):
+    """The bench's e2e loop: two sessions on their own streams, session B
+    loading (host flatten + H2D) while session A evaluates, B's evaluate
+    ordered after A's by an event. Each step's rows must equal a
+    single-session evaluation of the same space."""
+    import torch
+    from paper_2411_14458_b200.planner import Planner
+
+    spaces = []
+    for seed in (1, 2):
+        topos, scens = workloads.config2(2_000, seed=seed)
+        tarr, sarr = abi.array(abi.Topology, topos), abi.array(abi.Scenario, scens)
+        planner.load(tarr, sarr)
+        planner.evaluate()
+        spaces.append((tarr, sarr, [bytes(r) for r in planner.rows()]))
+    other = Planner(0)
+    try:
+        sessions = [planner, other]
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        for p, s in zip(sessions, streams):
+            p.set_stream(s.cuda_stream)
+        prev, pending = None, []
+        for i in range(6):
+            p, s = sessions[i % 2], streams[i % 2]
+            tarr, sarr, want = spaces[(i // 2) % 2]
+            p.load(tarr, sarr)
+            if prev is not None:
+                s.wait_event(prev)
+            p.evaluate(sync=False)
+            prev = torch.cuda.Event()
+            prev.record(s)
+            pending.append((p, want))
+            if len(pending) == 2:
+                q, w = pending.pop(0)
+                out = (abi.Row * q.n_rows)()
+                assert q.lib.gpb_fetch_rows(q.ctx, out, q.n_rows) == 0
+                assert [bytes(r) for r in out] == w, i
+        q, w = pending.pop(0)
+        assert [bytes(r) for r in q.rows()] == w
+    finally:
+        other.close()
+        planner.set_stream(None)
