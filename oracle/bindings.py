@@ -64,6 +64,9 @@ class Checker:
             self._whatif = f("whatif_count", C.c_int,
                              [P(abi.Topology), P(abi.Scenario), C.c_int32,
                               P(C.c_int64), P(C.c_int64)])
+            self._report = f("report_rows", C.c_int,
+                             [P(abi.Topology), P(abi.Scenario), C.c_int32,
+                              P(C.c_double), P(C.c_int64)])
         else:
             self._timeline_orc = f("timeline", C.c_int,
                                    [P(abi.Topology), P(abi.Scenario), C.c_int32,
@@ -145,6 +148,18 @@ class Checker:
         out = (abi.Request * max(1, count))()
         self._check(self._synth(count, seed, horizon_ms, C.byref(pm), out))
         return list(out[:count])
+
+    def report_rows(self, topos, sc, n):
+        """[(utilization, makespan_ns)] of rows d = 1..n: the reference's
+        report() on run() (metrics.cpp:39-54); (0, 0) for infeasible rows.
+        The port's select() rows carry the same two values."""
+        if self.prefix != "ref":
+            rows, _, _ = self.select(topos, sc)
+            return [(r.utilization, r.makespan_ns) for r in rows[:n]]
+        util = (C.c_double * max(1, n))()
+        mk = (C.c_int64 * max(1, n))()
+        self._check(self._report(topos, C.byref(sc), n, util, mk))
+        return list(zip(util[:n], mk[:n]))
 
     def whatif_count(self, topos, scens):
         arr = abi.array(abi.Scenario, scens)

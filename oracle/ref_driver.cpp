@@ -252,6 +252,25 @@ int ref_utilization(const gpb_topology* topos, const gpb_scenario* sc,
   });
 }
 
+// report() on the run() timeline of every row d = 1..n of one scenario:
+// mean utilization (metrics.cpp:39-54) and makespan (schedule.cpp:42-44);
+// infeasible rows (InsufficientGpus) get 0 / 0 like gpb_row.
+int ref_report_rows(const gpb_topology* topos, const gpb_scenario* sc,
+                    int32_t n, double* util, int64_t* makespan) {
+  return guarded([&] {
+    for (int d = 1; d <= n; ++d) {
+      util[d - 1] = 0.0;
+      makespan[d - 1] = 0;
+      try {
+        Timeline tl = timeline_of(topos, *sc, d, 1, nullptr, nullptr);
+        util[d - 1] = report(tl).mean_utilization;
+        makespan[d - 1] = tl.makespan;
+      } catch (const InsufficientGpus&) {
+      }
+    }
+  });
+}
+
 int ref_bubbles(const gpb_topology* topos, const gpb_scenario* sc, int32_t d,
                 int64_t horizon, gpb_bubble* out, int64_t cap, int64_t* n) {
   return guarded([&] {

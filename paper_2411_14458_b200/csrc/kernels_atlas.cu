@@ -13,8 +13,8 @@
 // Forward phase (scheduler.cpp:362-431): memory-cap admission first. The
 // reference drains "the deepest stage with a ready pair" one pair at a time;
 // draining stage s never readies a deeper stage, so an admission is one
-// descending pass over the stages, run by lane 0 with the stage-above state
-// forwarded in registers. The chain of one microbatch is then a max-plus map
+// descending pass over the stages, evaluated in rounds of warp suffix scans
+// (atlas_cascade, lane = stage). The chain of one microbatch is then a max-plus map
 // of its start t0: e_s(t0) = a_s + f + max(t0, G_s), a_s = s*f + sum of the
 // WAN (ser + lat) below s, G_s = max_{j<=s}(gpu_free_j - a_j) (warp
 // max-scan), so the exact-fit shift loop touches only the WAN boundaries.
@@ -22,9 +22,9 @@
 // Drain (scheduler.cpp:452-505): the global greedy commits pairs in
 // non-decreasing start time and stage s depends only on itself, its private
 // gradient link and the gradient arrivals of stage s+1; it equals a per-stage
-// greedy. Lanes run those per-stage greedies as a lock-step
-// wavefront: stage s commits its best (t, p) only if t < last_commit(s+1) +
-// pair_dur, the earliest any later gradient from s+1 can arrive.
+// greedy, run from stage S-1 down: a WAN stage as a warp
+// argmin over its pipelines (lane = pipeline), a run of stages without a WAN
+// gradient link as segmented prefix-max scans or one 2-D wavefront.
 //
 // Right-pack (scheduler.cpp:506-529) runs only in the timeline variant.
 #include <cuda_runtime.h>
@@ -277,7 +277,7 @@ constexpr long long kNegMP = -(1LL << 53);
 
 __device__ __forceinline__ long long mp_add(long long x, long long y) { return x + y; }
 
-template <int B, bool TIMELINE>
+template <int B, bool TIMELINE, bool PROF>
 __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L, AtlasMem& X,
                                               long long (&gfr)[B], int (&drr)[B],
                                               const int (&wbi)[B], const long long (&serb)[B],
@@ -290,7 +290,7 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
   // ownb[j]: start of pipeline p's last reservation on stage j's gradient
   // link (its own list tail); mcur/mn: cursor into / size of the link's
   // static merged list — register copies, one lane owns each stage
-  long long ct = cph ? clock64() : 0;
+  long long ct = PROF ? clock64() : 0;
   const int lane = threadIdx.x & 31;
   const int S = g.S, M = g.M, C = g.C;
   const int nl = (S + B - 1) / B;  // lanes owning stages
@@ -315,7 +315,7 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
     nmax = max(nmax, cnt[j]);
   }
   const int R = __reduce_max_sync(kFull, nmax);
-  if (cph) {
+  if (PROF) {
     int tot = 0;
 #pragma unroll
     for (int j = 0; j < B; ++j) tot += cnt[j];
@@ -325,8 +325,8 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
 #pragma unroll
   for (int j = 0; j < B; ++j) wl[j] = wbi[j] >= 0 ? serb[j] + latb[j] : 0;
 
-  n_rounds += R;
-  if (cph) {
+  if (PROF) n_rounds += R;
+  if (PROF) {
     const long long t1 = clock64();
     cph[0] += t1 - ct;
     ct = t1;
@@ -344,7 +344,7 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
       }
     }
     long long lo[B];
-    if (cph) {
+    if (PROF) {
       const long long t1 = clock64();
       cph[1] += t1 - ct;
       ct = t1;
@@ -382,7 +382,7 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
 #pragma unroll
     for (int j = 0; j < B; ++j) DLs[j] = 0;
     for (;;) {
-      ++n_scans;
+      if (PROF) ++n_scans;
       long long um[B], run = kNegMP;
 #pragma unroll
       for (int j = B - 1; j >= 0; --j) {
@@ -435,7 +435,7 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
           if (lane * B + j <= sw) DLs[j] += shift;
       }
     }
-    if (cph) {
+    if (PROF) {
       const long long t1 = clock64();
       cph[2] += t1 - ct;
       ct = t1;
@@ -457,7 +457,7 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
       if (TIMELINE) X.ps[((size_t)p * S + s) * M + k] = t;
     }
     __syncwarp();
-    if (cph) {
+    if (PROF) {
       const long long t1 = clock64();
       cph[3] += t1 - ct;
       ct = t1;
@@ -719,7 +719,9 @@ __device__ void drain_stage_greedy(const Geom& g, AtlasMem& X, int s, int w) {
 
 constexpr int kWaveRatio = 8;
 
-template <int B, bool TIMELINE>
+// PROF: per-row phase counters (gpb_set_profile; a separate instantiation,
+// so the production kernel carries no clock reads or counters)
+template <int B, bool TIMELINE, bool PROF>
 __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& err,
                                long long* phase = nullptr) {
   const int lane = threadIdx.x & 31;
@@ -867,19 +869,18 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     }
     for (int m = 0; m < M; ++m) {
       // memory-cap admission (:366-381) + forced drains (:321-346)
-      if (phase) ph_t = clock64();
+      if (PROF) ph_t = clock64();
       int nblk = 0;
 #pragma unroll
       for (int j = 0; j < B; ++j)
         if (lane * B + j < S && m - drr[j] >= mem_limit) ++nblk;
-#pragma unroll
       nblk = __reduce_add_sync(kFull, nblk);
       if (nblk > 0) {
-        atlas_cascade<B, TIMELINE>(g, p, m, mem_limit, X, gfr, drr, wbi, serb, latb, ownb, mcur,
-                                   mn, wsuf, n_pairs, n_stage_it, n_rounds, phase ? cph : nullptr);
-        ++n_adm;
+        atlas_cascade<B, TIMELINE, PROF>(g, p, m, mem_limit, X, gfr, drr, wbi, serb, latb, ownb,
+                                         mcur, mn, wsuf, n_pairs, n_stage_it, n_rounds, cph);
+        if (PROF) ++n_adm;
       }
-      if (phase) {
+      if (PROF) {
         const long long t1 = clock64();
         ph_casc += t1 - ph_t;
         ph_t = t1;
@@ -912,7 +913,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
         if (lane < nw) gw = X.wg[lane];
       }
       long long t0 = __shfl_sync(kFull, gfr[0], 0);  // gpu_free of stage 0
-      if (phase) {
+      if (PROF) {
         const long long t1 = clock64();
         ph_chain += t1 - ph_t;
         ph_t = t1;
@@ -937,7 +938,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
           X.resf[((size_t)lane * C + p) * M + m] = ownw_l;
         }
       }
-      if (phase) {
+      if (PROF) {
         const long long t1 = clock64();
         ph_fit += t1 - ph_t;
         ph_t = t1;
@@ -965,7 +966,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     __syncwarp();
   }
 
-  if (phase) ph_t = clock64();
+  if (PROF) ph_t = clock64();
   // ------------------------------------------ drain: stage by stage
   // Pairs drained by the forward phase are excluded from the right-pack.
   for (int i = lane; i < C * S; i += 32) X.firstm[i] = X.nm[i];
@@ -981,12 +982,12 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
   }
   long long dph[4] = {0, 0, 0, 0};  // drain: greedy / scan / wavefront cycles, wave steps
   for (int s = S - 1; s >= 0;) {
-    const long long td = phase ? clock64() : 0;
+    const long long td = PROF ? clock64() : 0;
     const int w = X.wbs[s];
     if (w >= 0) {
       drain_stage_greedy<TIMELINE>(g, X, s, w);
       --s;
-      if (phase) dph[0] += clock64() - td;
+      if (PROF) dph[0] += clock64() - td;
       continue;
     }
     int sb = s;  // the run of stages without a WAN gradient link below s
@@ -996,19 +997,19 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     const int R = s - sb + 1, CM = C * g.M;
     if ((long long)(CM + (R + B - 1) / B) > (long long)kWaveRatio * R * ((CM + 255) / 256)) {
       for (; s >= sb; --s) drain_stage_scan<TIMELINE>(g, X, s);
-      if (phase) dph[1] += clock64() - td;
+      if (PROF) dph[1] += clock64() - td;
       continue;
     }
     constexpr int BW = B < 4 ? B : 4;  // stages per lane (register arrays)
     for (int st = s; st >= sb; st -= 32 * BW) {
       const int bot = max(sb, st - 32 * BW + 1), rr = st - bot + 1;
       drain_run_wavefront<BW, TIMELINE>(g, X, st, bot);
-      dph[3] += CM + (rr + BW - 1) / BW;
+      if (PROF) dph[3] += CM + (rr + BW - 1) / BW;
     }
     s = sb - 1;
-    if (phase) dph[2] += clock64() - td;
+    if (PROF) dph[2] += clock64() - td;
   }
-  if (phase && lane == 0) {
+  if (PROF && lane == 0) {
     ph_drain = clock64() - ph_t;
     phase[0] = ph_casc;
     phase[1] = ph_chain;
@@ -1066,7 +1067,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
 #define GPB_ATLAS_MIN_BLOCKS_B1 3
 #endif
 
-template <int B>
+template <int B, bool PROF>
 __global__ void __launch_bounds__(kEvalThreads, B == 1 ? GPB_ATLAS_MIN_BLOCKS_B1 : 1)
     atlas_kernel(EvalArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1086,8 +1087,9 @@ __global__ void __launch_bounds__(kEvalThreads, B == 1 ? GPB_ATLAS_MIN_BLOCKS_B1
     const DevTopo* tp;
     if (!begin_row(a, row, g, sc, tp)) continue;
     int err = 0;
-    const long long mk = atlas_row<B, false>(g, sc->mem_limit, X, err,
-                                             a.row_phase ? a.row_phase + 16 * (size_t)row : nullptr);
+    const long long mk =
+        atlas_row<B, false, PROF>(g, sc->mem_limit, X, err,
+                                  PROF ? a.row_phase + 16 * (size_t)row : nullptr);
     end_row(a, row, g, *sc, *tp, mk, err, t_start);
     __syncwarp();
   }
@@ -1114,7 +1116,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) atlas_timeline_kernel(EvalArg
     X.fe = a.tl_fe + a.tl_off[wk];
     X.ps = a.tl_ps + a.tl_off[wk];
     int err = 0;
-    const long long mk = atlas_row<B, true>(g, sc->mem_limit, X, err);
+    const long long mk = atlas_row<B, true, false>(g, sc->mem_limit, X, err);
     end_row(a, row, g, *sc, *tp, mk, err, t_start);
     __syncwarp();
   }
@@ -1131,11 +1133,14 @@ static cudaError_t ensure_smem_attr(size_t smem) {
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(mu);
   if (dev < 64 && done[dev] >= (int)smem) return cudaSuccess;
-  const cudaError_t e =
+  cudaError_t e =
       TL ? cudaFuncSetAttribute(atlas_timeline_kernel<B>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-         : cudaFuncSetAttribute(atlas_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem);
+         : cudaFuncSetAttribute(atlas_kernel<B, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess && !TL)  // the profiling instantiation (gpb_set_profile)
+    e = cudaFuncSetAttribute(atlas_kernel<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
   if (e == cudaSuccess && dev < 64) done[dev] = (int)smem;
   return e;
 }
@@ -1168,7 +1173,10 @@ static cudaError_t launch_atlas_b(const EvalArgs& a, int grid, int wpc, cudaStre
   const size_t smem = (size_t)wpc * a.lay.total;
   cudaError_t e = ensure_smem_attr<B, false>(smem);
   if (e != cudaSuccess) return e;
-  atlas_kernel<B><<<grid, 32 * wpc, smem, st>>>(a);
+  if (a.row_phase)
+    atlas_kernel<B, true><<<grid, 32 * wpc, smem, st>>>(a);
+  else
+    atlas_kernel<B, false><<<grid, 32 * wpc, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -1182,7 +1190,7 @@ int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem) {
     if (e == cudaSuccess)                                                                   \
       e = timeline ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_timeline_kernel<BB>, \
                                                                    32 * wpc, smem)          \
-                   : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_kernel<BB>,    \
+                   : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_kernel<BB, false>, \
                                                                    32 * wpc, smem);         \
     break;
   switch (B) {

@@ -10,10 +10,10 @@
 //      progress counters by shuffle. The reference's program DAG has a unique
 //      timing, and under lock-step the producer is never more than one item
 //      ahead of its consumer (checked in-kernel; violation => error row).
-//  atlas_kernel            atlas (scheduler.cpp:276-538)
+//  atlas_kernel            atlas (scheduler.cpp:276-538), in kernels_atlas.cu
 //      forward chains via a warp max-plus scan and O(#WAN) exact-fit checks,
-//      memory-cap forced drains, then the global greedy drain with a cached
-//      candidate table and a three-step redux argmin per committed pair.
+//      memory-cap forced drains as rounds of warp suffix scans, then the
+//      drain stage by stage (per-stage greedy / prefix-max scans).
 //
 // Every kernel pulls rows from a per-bucket work list with an atomic cursor
 // (persistent warps) and finishes each row with finish_row() (all-reduce,

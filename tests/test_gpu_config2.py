@@ -1,8 +1,9 @@
 """GPU parity at BASELINE config 2's full size (the bench workload): every one
 of the 10^4 (scenario, D) rows of the Llama-3 70B plan search, all four
 policies, bit-exact against the reference's select() (oracle/_ref compiled
-from the reference sources, else the C port), plus the per-scenario choice
-and the global best. The reference runs on a host thread pool (its core is
+from the reference sources, else the C port), the reference's report() on
+run() for utilization and makespan, plus the per-scenario choice and the
+global best. The reference runs on a host thread pool (its core is
 re-entrant)."""
 from concurrent.futures import ThreadPoolExecutor
 import os
@@ -28,16 +29,25 @@ def test_config2_all_rows_bit_exact(planner, checker):
     rows = planner.rows()
     res = planner.scenario_results()
     order = sorted(range(len(scens)), key=lambda i: -scens[i].num_microbatches * scens[i].d_max)
+
+    def ref_scenario(i):
+        # select() rows, plus report() on run() for every row: utilization
+        # (metrics.cpp:39-54) and makespan (schedule.cpp:42-44)
+        return checker.select(tarr, scens[i]), checker.report_rows(tarr, scens[i],
+                                                                   scens[i].d_max)
+
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
-        ref = dict(zip(order, ex.map(lambda i: checker.select(tarr, scens[i]), order)))
+        ref = dict(zip(order, ex.map(ref_scenario, order)))
     best = (-1.0, -1)
     for i, sc in enumerate(scens):
-        ref_rows, chosen, used = ref[i]
+        (ref_rows, chosen, used), rep = ref[i]
         r0 = res[i].first_row
         assert (res[i].n_rows, res[i].chosen_d, res[i].gpus_used) == (len(ref_rows), chosen, used)
-        for k, b in enumerate(ref_rows):
+        for k, (b, (util, mk)) in enumerate(zip(ref_rows, rep)):
             a = rows[r0 + k]
             assert _key(a) == _key(b), (i, k + 1, abi.POLICY_NAMES[sc.policy], _key(a), _key(b))
+            assert (a.utilization, a.makespan_ns) == (util, mk), \
+                (i, k + 1, abi.POLICY_NAMES[sc.policy], a.utilization, util, a.makespan_ns, mk)
             if b.feasible == 1 and b.throughput > best[0]:
                 best = (b.throughput, r0 + k)
     got = planner.best()

@@ -20,27 +20,33 @@ def _row_key(r):
 
 
 def _compare_space(planner, checker, port, topos, scens):
+    """Every row of the space vs the checker's select(), and utilization /
+    makespan vs its report() on run() (the reference's, metrics.cpp:39-54,
+    when oracle/_ref is present; else the C port's rows, pinned to the
+    reference in test_oracle.py). `port` is kept for call compatibility."""
+    from concurrent.futures import ThreadPoolExecutor
+    import os
     planner.load(topos, scens)
     planner.evaluate()
     rows = planner.rows()
     res = planner.scenario_results()
+
+    def ref_scenario(i):
+        sel = checker.select(topos, scens[i])
+        return sel, checker.report_rows(topos, scens[i], len(sel[0]))
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        ref = list(ex.map(ref_scenario, range(len(scens))))
     n_checked = 0
-    for i, sc in enumerate(scens):
-        ref_rows, chosen, used = checker.select(topos, sc)
-        # utilization/makespan come from the C port (the reference's select()
-        # has no utilization; the port's equals report() on run(), pinned in
-        # test_oracle_vs_ref.py)
-        port_rows, _, _ = port.select(topos, sc)
+    for i, ((ref_rows, chosen, used), rep) in enumerate(ref):
         r0 = res[i].first_row
         assert res[i].n_rows == len(ref_rows)
         assert res[i].chosen_d == chosen, f"scenario {i}"
         assert res[i].gpus_used == used
-        for k, (a, b, c) in enumerate(zip(rows[r0:r0 + len(ref_rows)], ref_rows, port_rows)):
+        for k, (a, b, (util, mk)) in enumerate(zip(rows[r0:r0 + len(ref_rows)], ref_rows, rep)):
             assert a.scenario == i
             assert _row_key(a) == _row_key(b), f"scenario {i} d={k+1}: {_row_key(a)} vs {_row_key(b)}"
-            if a.feasible:
-                assert a.makespan_ns == c.makespan_ns
-                assert a.utilization == c.utilization, (i, k, a.utilization, c.utilization)
+            assert (a.makespan_ns, a.utilization) == (mk, util), (i, k, a.utilization, util)
             n_checked += 1
     return n_checked
 
@@ -69,6 +75,24 @@ def test_config1_kats(planner):
         topos, sc = fixtures.config1(pol, multi)
         got = planner.select(topos, sc).rows[0].pp_time_ms
         assert abs(got - ms) < 5e-7, (pol, multi, got)
+
+
+def test_config1_bit_exact(planner, checker):
+    """BASELINE config 1 (4-stage PP over 2 DCs, M=8), all four policies x
+    single/multi TCP: the whole row (pp/all-reduce/total/throughput doubles,
+    partitions, chosen) bit-exact against the reference's select()
+    (dc_select.cpp:99-123) and utilization/makespan against its report() on
+    run() (metrics.cpp:39-54)."""
+    for pol in ("gpipe", "1f1b", "varuna", "atlas"):
+        for multi in (False, True):
+            topos, sc = fixtures.config1(pol, multi)
+            rep = planner.select(topos, sc)
+            ref_rows, chosen, used = checker.select(topos, sc)
+            assert rep.chosen_d == chosen and rep.gpus_used == used, (pol, multi)
+            (util, mk), = checker.report_rows(topos, sc, 1)
+            a, b = rep.rows[0], ref_rows[0]
+            assert _row_key(a) == _row_key(b), (pol, multi, _row_key(a), _row_key(b))
+            assert (a.utilization, a.makespan_ns) == (util, mk), (pol, multi)
 
 
 def test_small_random_spaces(planner, checker):

@@ -2,7 +2,8 @@
 3 (Llama-3.1 405B over 5 DCs, 10^6 rows evaluated in one launch sequence) and
 random ATLAS stress shapes (up to 126 stages = 4 stages per lane, 256
 microbatches, 8 pipelines, small memory caps), every sampled row bit-exact
-against the reference's select()."""
+against the reference's select(), utilization and makespan against its
+report() on run()."""
 from concurrent.futures import ThreadPoolExecutor
 import os
 import random
@@ -23,14 +24,21 @@ def _check_sample(planner, checker, topos, scens, idx):
     tarr = abi.array(abi.Topology, topos)
     rows = planner.rows()
     res = planner.scenario_results()
+    def ref_scenario(i):
+        sel = checker.select(tarr, scens[i])
+        return sel, checker.report_rows(tarr, scens[i], len(sel[0]))
+
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
-        ref = list(ex.map(lambda i: checker.select(tarr, scens[i]), idx))
+        ref = list(ex.map(ref_scenario, idx))
     n = 0
-    for i, (ref_rows, chosen, used) in zip(idx, ref):
+    for i, ((ref_rows, chosen, used), rep) in zip(idx, ref):
         r0 = res[i].first_row
         assert (res[i].n_rows, res[i].chosen_d, res[i].gpus_used) == (len(ref_rows), chosen, used), i
-        for k, b in enumerate(ref_rows):
-            assert _key(rows[r0 + k]) == _key(b), (i, k + 1, abi.POLICY_NAMES[scens[i].policy])
+        for k, (b, (util, mk)) in enumerate(zip(ref_rows, rep)):
+            a = rows[r0 + k]
+            assert _key(a) == _key(b), (i, k + 1, abi.POLICY_NAMES[scens[i].policy])
+            # report() on run(): utilization and makespan (metrics.cpp:39-54)
+            assert (a.utilization, a.makespan_ns) == (util, mk), (i, k + 1)
             n += 1
     return n
 
