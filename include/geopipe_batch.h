@@ -263,8 +263,9 @@ typedef struct gpb_timing {
 int gpb_get_timing(gpb_ctx* ctx, gpb_timing* out);
 
 /* On-device issue-rate microbenchmark used as the roofline denominator:
- * kind 0 = int64 max-plus ops (one max or one add = 1 op) in independent
- * register chains over every SM. Returns Gop/s. */
+ * max-plus ops (one max or one add = 1 op) in independent register chains
+ * over every SM; kind 0 = int64 (the kernels' representation), 1 = FP64
+ * holding exact integers (DADD/DMNMX), 2 = int32. Returns Gop/s. */
 int gpb_microbench(gpb_ctx* ctx, int32_t kind, double* gops);
 
 /* Per-bucket timing events in gpb_evaluate (default on: gpb_get_timing's
@@ -286,6 +287,33 @@ typedef struct gpb_bucket_info {
   double algo_ops;             /* algorithmic max-plus ops of its feasible rows */
 } gpb_bucket_info;
 int gpb_bucket_infos(gpb_ctx* ctx, gpb_bucket_info* out, int32_t cap, int32_t* n);
+
+/* ---------------------------------------------------------------------
+ * One plan space over several GPUs of one box (the batch
+ * behind whatif(), dc_select.cpp:125-134, as run_whatif calls it,
+ * runner.cpp:112-122). Whole scenarios are dealt to the devices by estimated
+ * cost (longest first onto the least-loaded device); each device's context
+ * is driven from its own host thread; the per-device winners (16 bytes) are
+ * exchanged with one ncclAllGather over NVLink (NCCL opened at run time).
+ * Rows, scenario results and the winner come back in the order of the whole
+ * space and equal a single-device evaluation bit for bit.
+ * --------------------------------------------------------------------- */
+typedef struct gpb_group gpb_group;
+
+/* Contexts on `devices[0..n_dev)` (n_dev <= 0: every visible device). A
+ * device listed twice gets two contexts (the winners then go through the
+ * host instead of NCCL). NULL on failure. */
+gpb_group* gpb_group_create(int32_t n_dev, const int32_t* devices);
+void gpb_group_destroy(gpb_group* g);
+const char* gpb_group_last_error(gpb_group* g);
+int32_t gpb_group_size(gpb_group* g);
+int gpb_group_load(gpb_group* g, const gpb_topology* topos, int32_t n_topo,
+                   const gpb_scenario* scens, int32_t n_scen, int64_t* n_rows);
+/* Evaluate every shard and all-gather the per-device winners (async). */
+int gpb_group_evaluate(gpb_group* g);
+int gpb_group_fetch_rows(gpb_group* g, gpb_row* rows, int64_t n_rows);
+int gpb_group_fetch_scenarios(gpb_group* g, gpb_scenario_result* out, int32_t n_scen);
+int gpb_group_fetch_best(gpb_group* g, gpb_best* out);
 
 #ifdef __cplusplus
 } /* extern "C" */

@@ -1079,7 +1079,7 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
       c.set_error("row index out of range");
       return GPB_CONFIG_ERROR;
     }
-    const int si = c.row_scen_host[rows[i]];
+    const int si = c.scen_of_row(rows[i]);
     const DevScen& sc = c.dev_scens_host[si];
     const DevTopo& tp = c.dev_topos_host[sc.topo];
     const int d = (int)(rows[i] - sc.first_row) + 1;
@@ -1145,7 +1145,7 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
     for (int B = 1; B <= 8; ++B) {
       Grp g{pol, B, (int)work.size(), 0, 0, 0, 0, 0};
       for (int i = 0; i < n; ++i) {
-        const DevScen& sc = c.dev_scens_host[c.row_scen_host[rows[i]]];
+        const DevScen& sc = c.dev_scens_host[c.scen_of_row(rows[i])];
         if (sc.policy != pol || (sc.S + 31) / 32 != B) continue;
         work.push_back((int32_t)rows[i]);
         offs.push_back(slots[i].tl_off);
@@ -1242,7 +1242,7 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
 namespace gpb {
 // WAN boundaries of a row's plan (DC blocks - 1), or -1 if infeasible.
 int row_wan_boundaries(const Ctx& c, int64_t row) {
-  const int si = c.row_scen_host[row];
+  const int si = c.scen_of_row(row);
   const DevScen& sc = c.dev_scens_host[si];
   const HostBlocks hb = host_decode(sc, c.dev_topos_host[sc.topo], (int)(row - sc.first_row) + 1);
   return hb.feasible ? hb.nb - 1 : -1;
@@ -1281,7 +1281,7 @@ extern "C" int gpb_bubbles(gpb_ctx* ctx_, int64_t row, int64_t horizon_ns, gpb_b
   }
   // expand to every timeline GPU in id order (extract_bubbles sorts by GPU):
   // DCs in topology order; inside a DC ids go (cell, pipeline, stage).
-  const DevScen& sc = c.dev_scens_host[c.row_scen_host[row]];
+  const DevScen& sc = c.dev_scens_host[c.scen_of_row(row)];
   const DevTopo& tp = c.dev_topos_host[sc.topo];
   HostBlocks hb = host_decode(sc, tp, s.D);
   int64_t k = 0;
@@ -1343,7 +1343,8 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
       return GPB_CONFIG_ERROR;
     }
   cudaSetDevice(c.device);
-  cudaEventRecord(c.ev0, c.stream);
+  // its own event pair: evaluate's ev0..ev2 stay valid for gpb_get_timing
+  cudaEventRecord(c.pack_ev0, c.stream);
   std::vector<TlSlot> slots;
   int rc = build_timelines(c, rows, n_rows_sel, horizon_ns, slots, c.pack_allreduce);
   if (rc != GPB_OK) return rc;
@@ -1491,7 +1492,12 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
       ++n_heavy;
     if (n_heavy > 0) {
       if (!c.pack_side) {
-        cudaStreamCreateWithFlags(&c.pack_side, cudaStreamNonBlocking);
+        // highest priority: the block scheduler then starts every heavy CTA
+        // before the light kernel's queued CTAs (launch order alone across
+        // two streams is not honoured: the heavy plans set the kernel time)
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        cudaStreamCreateWithPriority(&c.pack_side, cudaStreamNonBlocking, hi);
         cudaEventCreateWithFlags(&c.pack_fork, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&c.pack_join, cudaEventDisableTiming);
       }
@@ -1511,7 +1517,7 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
     if (e != cudaSuccess) return c.cuda_fail(e, "pack launch");
     int32_t ovf = 0;
     cudaMemcpyAsync(&ovf, overflow, 4, cudaMemcpyDeviceToHost, st);
-    cudaEventRecord(c.ev3, st);
+    cudaEventRecord(c.pack_ev1, st);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return c.cuda_fail(e, "pack");
     if (a.stats) {
       std::vector<long long> hs(8 * (size_t)n_rows_sel);
@@ -1544,9 +1550,9 @@ extern "C" int gpb_pack_prefills(gpb_ctx* ctx_, const int64_t* rows, int32_t n_r
       return GPB_ERROR;
     }
     pool *= 4;
-    cudaEventRecord(c.ev0, st);
+    cudaEventRecord(c.pack_ev0, st);
   }
-  cudaEventElapsedTime(&c.pack_ms, c.ev0, c.ev3);
+  cudaEventElapsedTime(&c.pack_ms, c.pack_ev0, c.pack_ev1);
   cudaMemcpyAsync(summaries, dsum, sizeof(gpb_pack_summary) * n_rows_sel, cudaMemcpyDeviceToHost, st);
   if (placements)
     cudaMemcpyAsync(placements, dpl, sizeof(gpb_placement) * (size_t)n_rows_sel * n_req,

@@ -12,8 +12,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
-#include <cstring>
 #include <cstdlib>
+#include <cstring>
 #include <exception>
 #include <filesystem>
 #include <fstream>
@@ -27,6 +27,8 @@
 #include <vector>
 
 #include <nlohmann/json.hpp>
+
+#include <cuda_runtime.h>
 
 #include "../../include/geopipe.h"
 #include "../../include/geopipe_batch.h"
@@ -547,6 +549,9 @@ struct Session {
   std::string selection_table;
   gpb_ctx* ctx = nullptr;
 
+  gpb_group* group = nullptr;
+  bool group_checked = false;
+
   gpb_ctx* device() {
     if (!ctx) {
       const char* env = std::getenv("GEOPIPE_DEVICE");
@@ -554,6 +559,41 @@ struct Session {
       if (!ctx) throw Internal("no CUDA device available for the B200 batch path");
     }
     return ctx;
+  }
+  // The devices a whatif / select_dc space is sharded over (gpb_group_*):
+  // GEOPIPE_DEVICES="all" or a comma list ("0,1,2,3"); unset = every visible
+  // device when there is more than one. nullptr = one device (device()).
+  gpb_group* devices() {
+    if (group_checked) return group;
+    group_checked = true;
+    const char* env = std::getenv("GEOPIPE_DEVICES");
+    std::vector<int32_t> list;
+    if (env && std::string(env) != "all") {
+      std::string cur;
+      for (const char* q = env;; ++q) {
+        if (*q == ',' || *q == 0) {
+          if (!cur.empty()) list.push_back(std::atoi(cur.c_str()));
+          cur.clear();
+          if (*q == 0) break;
+        } else {
+          cur += *q;
+        }
+      }
+      if (list.size() <= 1) return nullptr;
+    } else {
+      int n = 0;
+      if (cudaGetDeviceCount(&n) != cudaSuccess || n < 2) return nullptr;
+    }
+    group = gpb_group_create((int32_t)list.size(), list.empty() ? nullptr : list.data());
+    if (!group) throw Internal("GEOPIPE_DEVICES: could not open the device group");
+    return group;
+  }
+  void check_group(int rc) {
+    if (rc == GPB_OK) return;
+    const std::string msg = gpb_group_last_error(group);
+    if (rc == GPB_CONFIG_ERROR) throw ConfigError("", msg);
+    if (rc == GPB_INFEASIBLE) throw Infeasible(msg);
+    throw Internal(msg);
   }
   void check(int rc) {
     if (rc == GPB_OK) return;
@@ -563,6 +603,7 @@ struct Session {
     throw Internal(msg);
   }
   ~Session() {
+    if (group) gpb_group_destroy(group);
     if (ctx) gpb_destroy(ctx);
   }
 };
@@ -947,7 +988,6 @@ struct Selection {
 };
 
 std::vector<Selection> run_selection(Session& se, const std::vector<RunConfig>& cfgs) {
-  gpb_ctx* ctx = se.device();
   std::vector<gpb_topology> topos;
   std::vector<gpb_scenario> scens;
   for (size_t i = 0; i < cfgs.size(); ++i) {
@@ -956,12 +996,24 @@ std::vector<Selection> run_selection(Session& se, const std::vector<RunConfig>& 
     scens.push_back(selection_scenario(cfgs[i], (int)i));
   }
   int64_t n_rows = 0;
-  se.check(gpb_load(ctx, topos.data(), (int32_t)topos.size(), scens.data(), (int32_t)scens.size(), &n_rows));
-  se.check(gpb_evaluate(ctx, 1));
-  std::vector<gpb_row> rows(std::max<int64_t>(1, n_rows));
+  std::vector<gpb_row> rows;
   std::vector<gpb_scenario_result> res(std::max<size_t>(1, scens.size()));
-  se.check(gpb_fetch_rows(ctx, rows.data(), n_rows));
-  se.check(gpb_fetch_scenarios(ctx, res.data(), (int32_t)scens.size()));
+  if (gpb_group* g = se.devices()) {  // the space sharded over the devices
+    se.check_group(gpb_group_load(g, topos.data(), (int32_t)topos.size(), scens.data(),
+                                  (int32_t)scens.size(), &n_rows));
+    se.check_group(gpb_group_evaluate(g));
+    rows.resize(std::max<int64_t>(1, n_rows));
+    se.check_group(gpb_group_fetch_rows(g, rows.data(), n_rows));
+    se.check_group(gpb_group_fetch_scenarios(g, res.data(), (int32_t)scens.size()));
+  } else {
+    gpb_ctx* ctx = se.device();
+    se.check(gpb_load(ctx, topos.data(), (int32_t)topos.size(), scens.data(),
+                      (int32_t)scens.size(), &n_rows));
+    se.check(gpb_evaluate(ctx, 1));
+    rows.resize(std::max<int64_t>(1, n_rows));
+    se.check(gpb_fetch_rows(ctx, rows.data(), n_rows));
+    se.check(gpb_fetch_scenarios(ctx, res.data(), (int32_t)scens.size()));
+  }
   std::vector<Selection> out(scens.size());
   for (size_t i = 0; i < scens.size(); ++i) {
     out[i].rows.assign(rows.begin() + res[i].first_row, rows.begin() + res[i].first_row + res[i].n_rows);

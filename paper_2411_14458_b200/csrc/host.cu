@@ -17,6 +17,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/geopipe_batch.h"
@@ -114,6 +115,9 @@ Ctx::~Ctx() {
   if (ev1) cudaEventDestroy(ev1);
   if (ev2) cudaEventDestroy(ev2);
   if (ev3) cudaEventDestroy(ev3);
+  if (pack_ev0) cudaEventDestroy(pack_ev0);
+  if (pack_ev1) cudaEventDestroy(pack_ev1);
+  if (switch_ev) cudaEventDestroy(switch_ev);
   for (cudaEvent_t e : bucket_ev) cudaEventDestroy(e);
   for (cudaEvent_t e : bucket_ev_end) cudaEventDestroy(e);
   for (cudaEvent_t e : side_done) cudaEventDestroy(e);
@@ -195,6 +199,190 @@ static void validate_scenario(const gpb_scenario& s, int idx, int n_topo,
   if (act_bytes(s) <= 0) throw ConfigErr{"model: activation size overflow"};
 }
 
+
+// One scenario: validate (config.cpp / dc_select.cpp rules) and resolve it
+// into its DevScen (profile, order, d_max). Throws ConfigErr.
+static void flatten_scenario(const gpb_scenario& s, int i, int n_topo, const gpb_topology* topos,
+                             DevScen& d) {
+  validate_scenario(s, i, n_topo, topos);
+  const gpb_topology& t = topos[s.topology];
+  std::memset(&d, 0, sizeof d);
+  d.topo = s.topology;
+  d.policy = s.policy;
+  d.S = (s.num_layers + s.layers_per_partition - 1) / s.layers_per_partition;
+  d.M = s.num_microbatches;
+  d.C = s.pipelines_per_cell;
+  d.tp = s.tp_degree;
+  d.L = s.num_layers;
+  d.lpp = s.layers_per_partition;
+  d.recompute = s.recompute ? 1 : 0;
+  d.mem_limit = s.mem_limit > 0 ? s.mem_limit : d.S;  // scheduler.cpp:561
+  d.n_conns = s.multi_conn ? s.n_connections : 1;
+  d.bytes = act_bytes(s);
+  d.ppl = s.params_per_layer > 0 ? s.params_per_layer
+                                 : 12.0 * (double)s.hidden * (double)s.hidden;
+  if (s.ratio_C > 0) {  // from_ratio (workload.cpp:21-33)
+    const double comm_ms = (double)d.bytes / t.pair_bw_cap;
+    d.fwd_ms = comm_ms / s.ratio_C;
+    d.bwd_ms = 2.0 * d.fwd_ms;
+    d.rec_ms = d.fwd_ms;
+  } else {
+    d.fwd_ms = s.fwd_ms;
+    d.bwd_ms = s.bwd_ms;
+    d.rec_ms = s.recompute_ms;
+  }
+  if (d.policy == GPB_ATLAS) {
+    // the per-stage drain decomposition needs a positive pair duration
+    const long long dur = (long long)std::llround(d.bwd_ms * 1e6) +
+                          (d.recompute ? (long long)std::llround(d.rec_ms * 1e6) : 0);
+    if (dur <= 0)
+      throw ConfigErr{P_(i) + ": atlas pair duration rounds to 0 ns (outside the envelope)"};
+    // one lane per pipeline in the per-stage drain greedy
+    if (d.C > 32)
+      throw ConfigErr{P_(i) + ": atlas with more than 32 pipelines per cell is outside the "
+                              "kernel envelope"};
+  }
+  int order[GPB_MAX_DC];
+  int n_order = s.n_order;
+  if (n_order > 0) {
+    for (int k = 0; k < n_order; ++k) order[k] = s.dc_order[k];
+  } else {  // default_dc_order (workload.cpp:47-55): stable, count desc
+    n_order = t.n_dc;
+    for (int k = 0; k < n_order; ++k) order[k] = k;
+    std::stable_sort(order, order + n_order,
+                     [&](int a, int b) { return t.gpu_count[a] > t.gpu_count[b]; });
+  }
+  d.n_order = n_order;
+  for (int k = 0; k < n_order; ++k) d.order[k] = (int8_t)order[k];
+  long long total = 0;
+  for (int k = 0; k < t.n_dc; ++k) total += t.gpu_count[k];
+  const long long per_cell = (long long)d.C * d.S * d.tp;
+  const int dflt = (int)std::max<long long>(0, total / per_cell);  // dc_select.cpp:20-25
+  const int d_max = std::max(1, s.d_max > 0 ? s.d_max : dflt);
+  d.n_rows = d_max;
+}
+
+}  // namespace gpb
+
+namespace gpb {
+
+// Run fn(lo, hi) over [0, n) in contiguous chunks on up to 16 host threads
+// (one chunk when n is small).
+template <typename Fn>
+static void parallel_chunks(int64_t n, int64_t min_chunk, Fn fn) {
+  const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const int64_t nt = std::max<int64_t>(1, std::min<int64_t>({16, hw, n / std::max<int64_t>(1, min_chunk)}));
+  if (nt <= 1) {
+    fn(0, n, 0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int64_t t = 0; t < nt; ++t)
+    th.emplace_back([&, t] { fn(n * t / nt, n * (t + 1) / nt, (int)t); });
+  for (auto& x : th) x.join();
+}
+
+// Validate a plan space and flatten it into the device tables (DevTopo /
+// DevScen with resolved profile, order, d_max and first row; optionally the
+// row -> scenario table). Multi-threaded over topologies and scenarios for
+// large spaces; the error reported is the first one in input order
+// (topologies, then scenarios), as a sequential pass would find it.
+int flatten_space(const gpb_topology* topos, int32_t n_topo, const gpb_scenario* scens,
+                  int32_t n_scen, std::vector<DevTopo>& dt, std::vector<DevScen>& ds,
+                  std::vector<int32_t>* row_scen, int64_t& n_rows, std::string& err) {
+  if (n_scen < 0 || n_topo < 0 || (n_scen > 0 && (!topos || !scens))) {
+    err = "null input";
+    return GPB_CONFIG_ERROR;
+  }
+  dt.assign(std::max(n_topo, 1), DevTopo());
+  ds.assign(std::max(n_scen, 1), DevScen());
+  constexpr int kMaxThreads = 16;
+  // first error per chunk: (input index, message); topologies before scenarios
+  std::vector<std::pair<int64_t, std::string>> errs(kMaxThreads, {-1, ""});
+  auto first_error = [&]() -> const std::string* {
+    const std::pair<int64_t, std::string>* best = nullptr;
+    for (const auto& e : errs)
+      if (e.first >= 0 && (!best || e.first < best->first)) best = &e;
+    return best ? &best->second : nullptr;
+  };
+  parallel_chunks(n_topo, 2048, [&](int64_t lo, int64_t hi, int tid) {
+    // single_tcp_bandwidth (libm log/exp) per distinct latency of the default
+    // calibration table: plan spaces repeat a handful of WAN latencies
+    std::vector<std::pair<double, double>> tcp_memo;
+    auto single_bw = [&](const gpb_topology& t, double lat) {
+      if (t.n_tcp > 0) return gpb_single_tcp_bandwidth(&t, lat);
+      for (const auto& kv : tcp_memo)
+        if (kv.first == lat) return kv.second;
+      const double v = gpb_single_tcp_bandwidth(&t, lat);
+      tcp_memo.emplace_back(lat, v);
+      return v;
+    };
+    for (int64_t i = lo; i < hi; ++i) {
+      try {
+        validate_topology(topos[i], (int)i);
+      } catch (const ConfigErr& e) {
+        errs[tid] = {i, e.msg};
+        return;
+      }
+      const gpb_topology& t = topos[i];
+      DevTopo& d = dt[i];
+      std::memset(&d, 0, sizeof d);
+      d.n_dc = t.n_dc;
+      int base = 0;
+      for (int a = 0; a < t.n_dc; ++a) {
+        d.gpu_count[a] = t.gpu_count[a];
+        d.dc_base[a] = base;
+        base += t.gpu_count[a];
+        d.intra_bw[a] = t.intra_bw[a];
+        for (int b = 0; b < t.n_dc; ++b) {
+          // latency_between (topology.cpp:21-30): symmetric by unordered pair
+          const double lat = a == b ? 0.0 : t.latency_ms[std::min(a, b)][std::max(a, b)];
+          d.lat_ms[a][b] = lat;
+          d.single_bw[a][b] = single_bw(t, lat);
+        }
+      }
+      d.pair_cap = t.pair_bw_cap;
+    }
+  });
+  if (const std::string* e = first_error()) {
+    err = *e;
+    return GPB_CONFIG_ERROR;
+  }
+  parallel_chunks(n_scen, 4096, [&](int64_t lo, int64_t hi, int tid) {
+    for (int64_t i = lo; i < hi; ++i) {
+      try {
+        flatten_scenario(scens[i], (int)i, n_topo, topos, ds[i]);
+      } catch (const ConfigErr& e) {
+        errs[tid] = {n_topo + i, e.msg};
+        return;
+      }
+    }
+  });
+  if (const std::string* e = first_error()) {
+    err = *e;
+    return GPB_CONFIG_ERROR;
+  }
+  int64_t row = 0;
+  for (int i = 0; i < n_scen; ++i) {
+    ds[i].first_row = row;
+    row += ds[i].n_rows;
+    if (row > (int64_t)1 << 31) {
+      err = "plan space exceeds 2^31 rows";
+      return GPB_CONFIG_ERROR;
+    }
+  }
+  n_rows = row;
+  if (row_scen) {
+    row_scen->resize(row);
+    int32_t* rs = row_scen->data();
+    parallel_chunks(n_scen, 8192, [&](int64_t lo, int64_t hi, int) {
+      for (int64_t i = lo; i < hi; ++i)
+        std::fill(rs + ds[i].first_row, rs + ds[i].first_row + ds[i].n_rows, (int32_t)i);
+    });
+  }
+  return GPB_OK;
+}
+
 }  // namespace gpb
 
 // --------------------------------------------------------------- API
@@ -213,7 +401,9 @@ gpb_ctx* gpb_create(int device) {
   c->smem_optin = (int)prop.sharedMemPerBlockOptin;
   if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
-      cudaEventCreate(&c->ev2) != cudaSuccess || cudaEventCreate(&c->ev3) != cudaSuccess) {
+      cudaEventCreate(&c->ev2) != cudaSuccess || cudaEventCreate(&c->ev3) != cudaSuccess ||
+      cudaEventCreate(&c->pack_ev0) != cudaSuccess || cudaEventCreate(&c->pack_ev1) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->switch_ev, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return nullptr;
   }
@@ -231,6 +421,12 @@ const char* gpb_last_error(gpb_ctx* ctx) {
 static const bool kNoGroupFlush = std::getenv("GPB_NO_GROUP_FLUSH") != nullptr;
 // spaces with fewer rows keep one warp per flush row (GPB_GROUP_FLUSH_MIN_ROWS
 // overrides, read at every load: tests force the grouped kernel)
+// one-thread ATLAS rows: per-thread slice bound (int64 elements, 256 KB)
+constexpr long long kSeqMaxSlice = 32768;
+static int atlas_seq_mode() {
+  const char* e = std::getenv("GPB_ATLAS_SEQ");
+  return e ? std::atoi(e) : 1;
+}
 static int64_t group_flush_min_rows() {
   const char* e = std::getenv("GPB_GROUP_FLUSH_MIN_ROWS");
   return e ? std::atoll(e) : 200000;
@@ -260,114 +456,14 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
     c.set_error("null input");
     return GPB_CONFIG_ERROR;
   }
-  std::vector<DevTopo> dt(std::max(n_topo, 1));
-  std::vector<DevScen> ds(std::max(n_scen, 1));
-  std::vector<int32_t> row_scen;
-  // single_tcp_bandwidth (libm log/exp) per distinct latency of the default
-  // calibration table: plan spaces repeat a handful of WAN latencies
-  std::vector<std::pair<double, double>> tcp_memo;
-  auto single_bw = [&](const gpb_topology& t, double lat) {
-    if (t.n_tcp > 0) return gpb_single_tcp_bandwidth(&t, lat);
-    for (const auto& kv : tcp_memo)
-      if (kv.first == lat) return kv.second;
-    const double v = gpb_single_tcp_bandwidth(&t, lat);
-    tcp_memo.emplace_back(lat, v);
-    return v;
-  };
-  try {
-    for (int i = 0; i < n_topo; ++i) {
-      validate_topology(topos[i], i);
-      const gpb_topology& t = topos[i];
-      DevTopo& d = dt[i];
-      std::memset(&d, 0, sizeof d);
-      d.n_dc = t.n_dc;
-      int base = 0;
-      for (int a = 0; a < t.n_dc; ++a) {
-        d.gpu_count[a] = t.gpu_count[a];
-        d.dc_base[a] = base;
-        base += t.gpu_count[a];
-        d.intra_bw[a] = t.intra_bw[a];
-        for (int b = 0; b < t.n_dc; ++b) {
-          // latency_between (topology.cpp:21-30): symmetric by unordered pair
-          const double lat = a == b ? 0.0 : t.latency_ms[std::min(a, b)][std::max(a, b)];
-          d.lat_ms[a][b] = lat;
-          d.single_bw[a][b] = single_bw(t, lat);
-        }
-      }
-      d.pair_cap = t.pair_bw_cap;
-    }
-    int64_t row = 0;
-    for (int i = 0; i < n_scen; ++i) {
-      validate_scenario(scens[i], i, n_topo, topos);
-      const gpb_scenario& s = scens[i];
-      const gpb_topology& t = topos[s.topology];
-      DevScen& d = ds[i];
-      std::memset(&d, 0, sizeof d);
-      d.topo = s.topology;
-      d.policy = s.policy;
-      d.S = (s.num_layers + s.layers_per_partition - 1) / s.layers_per_partition;
-      d.M = s.num_microbatches;
-      d.C = s.pipelines_per_cell;
-      d.tp = s.tp_degree;
-      d.L = s.num_layers;
-      d.lpp = s.layers_per_partition;
-      d.recompute = s.recompute ? 1 : 0;
-      d.mem_limit = s.mem_limit > 0 ? s.mem_limit : d.S;  // scheduler.cpp:561
-      d.n_conns = s.multi_conn ? s.n_connections : 1;
-      d.bytes = act_bytes(s);
-      d.ppl = s.params_per_layer > 0 ? s.params_per_layer
-                                     : 12.0 * (double)s.hidden * (double)s.hidden;
-      if (s.ratio_C > 0) {  // from_ratio (workload.cpp:21-33)
-        const double comm_ms = (double)d.bytes / t.pair_bw_cap;
-        d.fwd_ms = comm_ms / s.ratio_C;
-        d.bwd_ms = 2.0 * d.fwd_ms;
-        d.rec_ms = d.fwd_ms;
-      } else {
-        d.fwd_ms = s.fwd_ms;
-        d.bwd_ms = s.bwd_ms;
-        d.rec_ms = s.recompute_ms;
-      }
-      if (d.policy == GPB_ATLAS) {
-        // the per-stage drain decomposition needs a positive pair duration
-        const long long dur = (long long)std::llround(d.bwd_ms * 1e6) +
-                              (d.recompute ? (long long)std::llround(d.rec_ms * 1e6) : 0);
-        if (dur <= 0)
-          throw ConfigErr{P_(i) + ": atlas pair duration rounds to 0 ns (outside the envelope)"};
-        // one lane per pipeline in the per-stage drain greedy
-        if (d.C > 32)
-          throw ConfigErr{P_(i) + ": atlas with more than 32 pipelines per cell is outside the "
-                                  "kernel envelope"};
-      }
-      int order[GPB_MAX_DC];
-      int n_order = s.n_order;
-      if (n_order > 0) {
-        for (int k = 0; k < n_order; ++k) order[k] = s.dc_order[k];
-      } else {  // default_dc_order (workload.cpp:47-55): stable, count desc
-        n_order = t.n_dc;
-        for (int k = 0; k < n_order; ++k) order[k] = k;
-        std::stable_sort(order, order + n_order,
-                         [&](int a, int b) { return t.gpu_count[a] > t.gpu_count[b]; });
-      }
-      d.n_order = n_order;
-      for (int k = 0; k < n_order; ++k) d.order[k] = (int8_t)order[k];
-      long long total = 0;
-      for (int k = 0; k < t.n_dc; ++k) total += t.gpu_count[k];
-      const long long per_cell = (long long)d.C * d.S * d.tp;
-      const int dflt = (int)std::max<long long>(0, total / per_cell);  // dc_select.cpp:20-25
-      const int d_max = std::max(1, s.d_max > 0 ? s.d_max : dflt);
-      d.first_row = row;
-      d.n_rows = d_max;
-      row += d_max;
-      if (row > (int64_t)1 << 31) throw ConfigErr{"plan space exceeds 2^31 rows"};
-    }
-    row_scen.resize(row);
-    for (int i = 0; i < n_scen; ++i)
-      for (int k = 0; k < ds[i].n_rows; ++k) row_scen[ds[i].first_row + k] = i;
-  } catch (const ConfigErr& e) {
-    c.last_error = e.msg;
-    return GPB_CONFIG_ERROR;
+  std::vector<DevTopo> dt;
+  std::vector<DevScen> ds;
+  int64_t n_rows = 0;
+  {
+    const int rc = flatten_space(topos, n_topo, scens, n_scen, dt, ds, nullptr, n_rows,
+                                 c.last_error);
+    if (rc != GPB_OK) return rc;
   }
-  const int64_t n_rows = (int64_t)row_scen.size();
 
   // Buckets: (policy, B = ceil(S/32)); within a bucket scenarios are dealt
   // in decreasing estimated cost so the persistent warps finish together.
@@ -395,21 +491,33 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   // keep fewer buckets (measured: config 2 0.59 -> 0.63 ms with the split,
   // config 5 387 -> 369 ms)
   const int64_t group_min = group_flush_min_rows();
-  auto gw_of = [&](const DevScen& d) {
-    if (d.policy == GPB_ATLAS || kNoGroupFlush || n_rows < group_min) return 32;
+  // ... and ATLAS rows of shallow pipelines (S <= 16) outside the heavy
+  // bucket run one per thread (atlas_seq_kernel); GPB_ATLAS_SEQ=0 disables,
+  // =2 also takes heavy rows (tests)
+  const int seq_mode = atlas_seq_mode();
+  auto seq_ok = [&](const DevScen& d, bool heavy) {
+    return seq_mode > 0 && n_rows >= group_min && d.S <= 16 && (!heavy || seq_mode == 2) &&
+           atlas_seq_slice(d.C, d.S, d.M, d.n_order - 1) <= kSeqMaxSlice;
+  };
+  auto gw_of = [&](const DevScen& d, bool heavy) {
+    if (d.policy == GPB_ATLAS) return seq_ok(d, heavy) ? 1 : 32;
+    if (kNoGroupFlush || n_rows < group_min) return 32;
     const int gw = d.S <= 8 ? 8 : (d.S <= 16 ? 16 : 32);
     // the per-row last-stage buffer (M entries per row) must fit the block
     return (size_t)(kEvalThreads / gw) * d.M * 8 <= 160 * 1024 ? gw : 32;
   };
   std::map<std::tuple<int, int, int, int>, std::vector<int>> by_key;
   for (int i = 0; i < n_scen; ++i) {
-    const int heavy = ds[i].policy == GPB_ATLAS && cost(i) >= 0.3 * max_atlas;
-    by_key[{ds[i].policy, (ds[i].S + 31) / 32, heavy, gw_of(ds[i])}].push_back(i);
+    int heavy = ds[i].policy == GPB_ATLAS && cost(i) >= 0.3 * max_atlas;
+    const int gw = gw_of(ds[i], heavy != 0);
+    if (gw == 1) heavy = 0;
+    by_key[{ds[i].policy, (ds[i].S + 31) / 32, heavy, gw}].push_back(i);
   }
-  std::vector<int32_t> work;
-  work.reserve(n_rows);
   std::vector<int32_t> bscen;
   bscen.reserve(n_scen);
+  std::vector<int64_t> bscen_row;  // work-list offset of each bscen entry's first row
+  bscen_row.reserve(n_scen);
+  int64_t n_work = 0;
   for (auto& [key, list] : by_key) {
     std::stable_sort(list.begin(), list.end(), [&](int a, int b) { return cost(a) > cost(b); });
     Bucket b;
@@ -417,11 +525,12 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
     b.B = std::get<1>(key);
     b.heavy = std::get<2>(key) != 0;
     b.gw = std::get<3>(key);
-    b.offset = (int32_t)work.size();
+    b.offset = (int32_t)n_work;
     double total = 0;
     for (int i : list) {
       total += cost(i) * ds[i].n_rows;
-      for (int k = 0; k < ds[i].n_rows; ++k) work.push_back((int32_t)(ds[i].first_row + k));
+      bscen_row.push_back(n_work);
+      n_work += ds[i].n_rows;
       b.max_m = std::max(b.max_m, ds[i].M);
       b.max_cs = std::max(b.max_cs, ds[i].C * ds[i].S);
       b.max_cm = std::max(b.max_cm, ds[i].C * ds[i].M);
@@ -430,7 +539,7 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
       b.max_s = std::max(b.max_s, ds[i].S);
       b.max_nw = std::max(b.max_nw, ds[i].n_order - 1);
     }
-    b.count = (int32_t)work.size() - b.offset;
+    b.count = (int32_t)(n_work - b.offset);
     b.scen_off = (int32_t)bscen.size();
     b.scen_cnt = (int32_t)list.size();
     for (int i : list) bscen.push_back(i);
@@ -452,11 +561,12 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
     c.sel_blocks += b.sel_grid;
   }
 
-  // Upload: the tables are staged in one pinned buffer and copied
-  // asynchronously on the launch stream (evaluate is ordered after them).
+  // Upload: the tables are written straight into one pinned staging buffer
+  // (the per-row tables by several host threads) and copied asynchronously
+  // on the launch stream (evaluate is ordered after them).
   cudaStream_t st = c.stream;
   const size_t sz_t = sizeof(DevTopo) * dt.size(), sz_s = sizeof(DevScen) * ds.size(),
-               sz_r = sizeof(int32_t) * row_scen.size(), sz_w = sizeof(int32_t) * work.size(),
+               sz_r = sizeof(int32_t) * n_rows, sz_w = sizeof(int32_t) * n_work,
                sz_b = sizeof(int32_t) * bscen.size();
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t stage_need = al(sz_t) + al(sz_s) + al(sz_r) + al(sz_w) + al(sz_b);
@@ -475,18 +585,34 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   if (!c.upload_ev && cudaEventCreateWithFlags(&c.upload_ev, cudaEventDisableTiming) != cudaSuccess)
     return c.cuda_fail(cudaGetLastError(), "event");
   unsigned char* sp = (unsigned char*)c.stage;
+  unsigned char* st_t = sp;
+  unsigned char* st_s = st_t + al(sz_t);
+  int32_t* st_r = (int32_t*)(st_s + al(sz_s));
+  int32_t* st_w = (int32_t*)((unsigned char*)st_r + al(sz_r));
+  int32_t* st_b = (int32_t*)((unsigned char*)st_w + al(sz_w));
+  std::memcpy(st_t, dt.data(), sz_t);
+  std::memcpy(st_s, ds.data(), sz_s);
+  std::memcpy(st_b, bscen.data(), sz_b);
+  // row -> scenario and the bucket work lists (rows of each bucket scenario
+  // in D order), one contiguous range of scenarios per host thread
+  parallel_chunks(n_scen, 8192, [&](int64_t lo, int64_t hi, int) {
+    for (int64_t i = lo; i < hi; ++i)
+      std::fill(st_r + ds[i].first_row, st_r + ds[i].first_row + ds[i].n_rows, (int32_t)i);
+    for (int64_t j = lo; j < hi; ++j) {
+      const DevScen& d = ds[bscen[j]];
+      int32_t* w = st_w + bscen_row[j];
+      for (int k = 0; k < d.n_rows; ++k) w[k] = (int32_t)(d.first_row + k);
+    }
+  });
   auto up = [&](Buf& b, const void* src, size_t bytes) -> bool {
     void* p = c.dev_buf(b, bytes);
     if (!p) return false;
     if (bytes == 0) return true;
-    std::memcpy(sp, src, bytes);
-    const bool ok = cudaMemcpyAsync(p, sp, bytes, cudaMemcpyHostToDevice, st) == cudaSuccess;
-    sp += al(bytes);
-    return ok;
+    return cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, st) == cudaSuccess;
   };
-  if (!up(c.b_topos, dt.data(), sz_t) || !up(c.b_scens, ds.data(), sz_s) ||
-      !up(c.b_row_scen, row_scen.data(), sz_r) || !up(c.b_work, work.data(), sz_w) ||
-      !up(c.b_bscen, bscen.data(), sz_b) ||
+  if (!up(c.b_topos, st_t, sz_t) || !up(c.b_scens, st_s, sz_s) ||
+      !up(c.b_row_scen, st_r, sz_r) || !up(c.b_work, st_w, sz_w) ||
+      !up(c.b_bscen, st_b, sz_b) ||
       !c.dev_buf(c.b_rows, sizeof(gpb_row) * std::max<int64_t>(n_rows, 1)) ||
       !c.dev_buf(c.b_results, sizeof(gpb_scenario_result) * std::max(n_scen, 1)) ||
       !c.dev_buf(c.b_cursors, sizeof(int32_t) * (c.buckets.size() + 1)) ||
@@ -496,22 +622,21 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   cudaEventRecord(c.upload_ev, st);
   c.upload_pending = true;
   c.d2h_bytes = 0;
-  c.h2d_bytes = sizeof(DevTopo) * dt.size() + sizeof(DevScen) * ds.size() +
-                sizeof(int32_t) * (row_scen.size() + work.size());
+  c.h2d_bytes = sz_t + sz_s + sz_r + sz_w + sz_b;
   c.n_rows = n_rows;
   c.n_scen = n_scen;
   c.n_topo = n_topo;
-  c.host_scens.assign(scens, scens + n_scen);
-  c.host_topos.assign(topos, topos + n_topo);
-  c.dev_scens_host = ds;
-  c.dev_topos_host = dt;
-  c.row_scen_host = row_scen;
-  c.work_host = work;
+  c.dev_scens_host = std::move(ds);
+  c.dev_topos_host = std::move(dt);
+  c.bscen_host = std::move(bscen);
   // the launch sequence (ATLAS shapes, scratch, stream assignment) depends
-  // only on the buckets' shapes: reuse it when a reload has the same ones
+  // only on the buckets' shapes: reuse it when a reload has the same ones.
+  // A captured graph (GPB_GRAPH) also bakes in the scenario split of each
+  // bucket's select launch and the table pointers (which a reload may
+  // reallocate), so it is re-captured after every load.
+  c.drop_graph();
   if (!same_shapes(prev_buckets, c.buckets)) {
     c.eval_ready = false;
-    c.drop_graph();
   } else {
     for (size_t i = 0; i < c.buckets.size(); ++i) c.buckets[i].stream = prev_buckets[i].stream;
   }
@@ -578,7 +703,7 @@ static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
       a.scratch_per_warp = P.scratch_per_warp;
       a.scratch_big_off = P.scratch_big_off;
       a.scratch = P.scratch_per_warp > 0 ? (long long*)c.b_scratch.ptr + c.scr_off[bi] : nullptr;
-      e = launch_atlas(b.B, a, P.grid, P.wpc, ss);
+      e = b.gw == 1 ? launch_atlas_seq(a, P.grid, ss) : launch_atlas(b.B, a, P.grid, P.wpc, ss);
     }
     if (e != cudaSuccess) return c.cuda_fail(e, "eval launch");
     if (bt) rec(c.bucket_ev_end[bi], ss);
@@ -651,6 +776,22 @@ static int prepare_evaluate(Ctx& c) {
   for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
     const Bucket& b = c.buckets[bi];
     if (b.policy != GPB_ATLAS || b.count == 0) continue;
+    if (b.gw == 1) {  // one thread per row: a [element][lane] slice per thread
+      AtlasPlan& P = c.aplan[bi];
+      const long long slice = atlas_seq_slice(b.max_c, b.max_s, b.max_m, b.max_nw);
+      P.wpc = kEvalThreads / 32;
+      const long long per_sm = std::max(1, atlas_seq_blocks_per_sm());
+      long long grid = std::min<long long>((long long)c.num_sms * per_sm,
+                                           (b.count + kEvalThreads - 1) / kEvalThreads);
+      // scratch bound: 12 GiB per bucket (rows beyond the resident ones reuse it)
+      while (grid > c.num_sms && grid * kEvalThreads * slice * 8 > (12LL << 30)) grid -= c.num_sms;
+      P.grid = (int)std::max(1LL, grid);
+      P.scratch_per_warp = 32 * slice;
+      P.scratch_big_off = 0;
+      c.scr_off[bi] = scr_total;
+      scr_total += (size_t)P.scratch_per_warp * P.grid * P.wpc;
+      continue;
+    }
     const int rc = plan_atlas(c, b.B, false, b.max_c, b.max_s, b.max_m, b.max_nw, b.max_csm,
                               b.count, c.aplan[bi]);
     if (rc != GPB_OK) return rc;
@@ -709,7 +850,7 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
   // every gpb_load re-captures (0.6 ms of host time per step in the e2e
   // loop) and the replayed step ran 15 % slower on the device than the
   // directly launched one (0.83 vs 0.71 ms).
-  static const bool use_graph = std::getenv("GPB_GRAPH") != nullptr;
+  const bool use_graph = std::getenv("GPB_GRAPH") != nullptr;
   if (!use_graph) {
     const int rc = record_evaluate(c, st, false);
     if (rc != GPB_OK) return rc;
@@ -805,8 +946,15 @@ int gpb_set_stream(gpb_ctx* ctx_, void* s) {
   if (!ctx_) return GPB_ERROR;
   Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
   cudaStream_t ns = s ? (cudaStream_t)s : c.own_stream;
-  // work on the new stream must see the last upload (async on the old one)
-  if (c.upload_pending && ns != c.stream) cudaStreamWaitEvent(ns, c.upload_ev, 0);
+  // work on the new stream is ordered after everything already enqueued on
+  // the old one (uploads, an evaluate or pack still running), so fetches on
+  // the new stream and the next load's H2D never overtake it
+  if (ns != c.stream) {
+    cudaSetDevice(c.device);
+    if (cudaEventRecord(c.switch_ev, c.stream) != cudaSuccess ||
+        cudaStreamWaitEvent(ns, c.switch_ev, 0) != cudaSuccess)
+      return c.cuda_fail(cudaGetLastError(), "set stream");
+  }
   c.stream = ns;
   return GPB_OK;  // the evaluate graph is re-captured for a new stream
 }
@@ -829,14 +977,15 @@ int gpb_bucket_infos(gpb_ctx* ctx_, gpb_bucket_info* out, int32_t cap, int32_t* 
     o.stream = b.stream;
     // algorithmic max-plus ops of the bucket's feasible rows
     double ops = 0;
-    for (int32_t k = 0; k < b.count; ++k) {
-      const int64_t row = c.work_host[b.offset + k];
-      const int W = row_wan_boundaries(c, row);
-      if (W < 0) continue;
-      const DevScen& d = c.dev_scens_host[c.row_scen_host[row]];
-      const double SM = (double)d.S * d.M, WM = (double)W * d.M;
-      ops += d.policy == GPB_ATLAS ? d.C * (4 * SM + 6 * WM)
-                                   : (d.policy == GPB_1F1B ? 4 * SM : 5 * SM) + 6 * WM;
+    for (int32_t j = 0; j < b.scen_cnt; ++j) {
+      const DevScen& d = c.dev_scens_host[c.bscen_host[b.scen_off + j]];
+      for (int32_t k = 0; k < d.n_rows; ++k) {
+        const int W = row_wan_boundaries(c, d.first_row + k);
+        if (W < 0) continue;
+        const double SM = (double)d.S * d.M, WM = (double)W * d.M;
+        ops += d.policy == GPB_ATLAS ? d.C * (4 * SM + 6 * WM)
+                                     : (d.policy == GPB_1F1B ? 4 * SM : 5 * SM) + 6 * WM;
+      }
     }
     o.algo_ops = ops;
     if (c.timing_valid && c.bucket_timing_valid) {
@@ -902,7 +1051,7 @@ int Ctx::check_error_flag() {
 extern "C" int gpb_microbench(gpb_ctx* ctx_, int32_t kind, double* gops) {
   if (!ctx_ || !gops) return GPB_ERROR;
   Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
-  if (kind != 0) {
+  if (kind < 0 || kind > 2) {
     c.set_error("unknown microbenchmark kind");
     return GPB_CONFIG_ERROR;
   }
@@ -911,18 +1060,17 @@ extern "C" int gpb_microbench(gpb_ctx* ctx_, int32_t kind, double* gops) {
   const int grid = c.num_sms * 8, iters = 4096;
   float best = 1e30f;
   for (int rep = 0; rep < 4; ++rep) {
-    cudaEventRecord(c.ev0, c.stream);
-    cudaError_t e = launch_maxplus_bench((long long*)out, grid, iters, c.stream);
+    cudaEventRecord(c.pack_ev0, c.stream);
+    cudaError_t e = launch_maxplus_bench(kind, (long long*)out, grid, iters, c.stream);
     if (e != cudaSuccess) return c.cuda_fail(e, "microbench");
-    cudaEventRecord(c.ev3, c.stream);
-    cudaEventSynchronize(c.ev3);
+    cudaEventRecord(c.pack_ev1, c.stream);
+    cudaEventSynchronize(c.pack_ev1);
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, c.ev0, c.ev3);
+    cudaEventElapsedTime(&ms, c.pack_ev0, c.pack_ev1);
     if (rep > 0 && ms < best) best = ms;
   }
   const double ops = (double)grid * 256 * iters * 8 * 2;
   *gops = ops / (best * 1e-3) / 1e9;
-  c.timing_valid = false;
   return GPB_OK;
 }
 

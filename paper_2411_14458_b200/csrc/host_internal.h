@@ -59,6 +59,8 @@ struct Ctx {
   cudaStream_t own_stream = nullptr; // the context's own stream
   int64_t d2h_bytes = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  cudaEvent_t pack_ev0 = nullptr, pack_ev1 = nullptr;  // gpb_pack_prefills / microbench
+  cudaEvent_t switch_ev = nullptr;                     // gpb_set_stream ordering
   std::string last_error;
 
   bool loaded = false;
@@ -66,12 +68,18 @@ struct Ctx {
   int32_t n_scen = 0, n_topo = 0;
   size_t h2d_bytes = 0;
   std::vector<Bucket> buckets;
-  std::vector<gpb_scenario> host_scens;
-  std::vector<gpb_topology> host_topos;
   std::vector<DevScen> dev_scens_host;
   std::vector<DevTopo> dev_topos_host;
-  std::vector<int32_t> row_scen_host;
-  std::vector<int32_t> work_host;  // bucket work lists (profiling)
+  std::vector<int32_t> bscen_host;  // bucket scenario lists (Bucket::scen_off / scen_cnt)
+  // scenario of a row: the last scenario whose first row is <= row
+  int32_t scen_of_row(int64_t row) const {
+    int32_t lo = 0, hi = n_scen;  // first scenario with first_row > row
+    while (lo < hi) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (dev_scens_host[mid].first_row <= row) lo = mid + 1; else hi = mid;
+    }
+    return lo - 1;
+  }
 
   // device tables
   Buf b_topos, b_scens, b_row_scen, b_work, b_rows, b_results, b_cursors, b_best, b_bscen;
@@ -138,5 +146,11 @@ int plan_atlas(Ctx& c, int B, bool timeline, int C, int S, int M, int nw, long l
                long long count, AtlasPlan& P);
 
 int row_wan_boundaries(const Ctx& c, int64_t row);
+
+// Validate + flatten a plan space on the host (multi-threaded for large
+// spaces); row_scen (nullable) receives the row -> scenario table.
+int flatten_space(const gpb_topology* topos, int32_t n_topo, const gpb_scenario* scens,
+                  int32_t n_scen, std::vector<DevTopo>& dt, std::vector<DevScen>& ds,
+                  std::vector<int32_t>* row_scen, int64_t& n_rows, std::string& err);
 
 }  // namespace gpb

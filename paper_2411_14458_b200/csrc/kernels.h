@@ -58,6 +58,11 @@ cudaError_t launch_onef1b(int B, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_onef1b_group(int gw, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_atlas(int B, const EvalArgs& a, int grid, int wpc, cudaStream_t st);
 int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem);
+// one thread per ATLAS row (bulk of large spaces); scratch_per_warp = 32 x
+// the per-thread slice (int64 elements) for rows up to (C, S, M, nw)
+long long atlas_seq_slice(int C, int S, int M, int nw);
+int atlas_seq_blocks_per_sm();
+cudaError_t launch_atlas_seq(const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_select(const SelectArgs& a, int grid, cudaStream_t st);
 // select_kernel alone (per bucket) / the final reduction of the block bests
 cudaError_t launch_select_part(const SelectArgs& a, int grid, cudaStream_t st);
@@ -68,5 +73,5 @@ cudaError_t launch_atlas_timeline(int B, const EvalArgs& a, int grid, int wpc, c
 }  // namespace gpb
 
 namespace gpb {
-cudaError_t launch_maxplus_bench(long long* out, int grid, int iters, cudaStream_t st);
+cudaError_t launch_maxplus_bench(int kind, long long* out, int grid, int iters, cudaStream_t st);
 }

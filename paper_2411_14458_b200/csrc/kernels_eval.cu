@@ -752,26 +752,41 @@ cudaError_t launch_best_reduce(const gpb_best* in, int n, gpb_best* out, cudaStr
 
 namespace gpb {
 
-// Peak int64 max-plus issue rate: 8 independent chains per thread of
-// x = max(x + a, y) (2 ops per update), every SM fully occupied.
-__global__ void __launch_bounds__(256) maxplus_bench_kernel(long long* out, int iters,
-                                                             long long a, long long y0) {
-  long long x[8];
+// Peak max-plus issue rate: 8 independent chains per thread of
+// x = max(x + a, c_k) (2 ops per update), every SM fully occupied, in the
+// three representations a max-plus recurrence on integer nanoseconds can use
+// (SURVEY.md Appendix D): int64 (INT32-pair IADD3/IADD3.X + compare/select),
+// exact-integer FP64 (DADD + DMNMX; exact while |t| < 2^53 ns) and int32
+// (IADD + IMNMX; range-limited, for comparison).
+template <typename T>
+__device__ __forceinline__ T mp_max(T a, T b) { return a > b ? a : b; }
+template <>
+__device__ __forceinline__ double mp_max<double>(double a, double b) { return fmax(a, b); }
+
+template <typename T>
+__global__ void __launch_bounds__(256) maxplus_bench_kernel(long long* out, int iters, T a, T y0) {
+  T x[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x + k;
-  long long y = y0 + blockIdx.x;
+  for (int k = 0; k < 8; ++k) x[k] = (T)(threadIdx.x + k);
+  const T y = y0 + (T)blockIdx.x;
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = imax(x[k] + a, y + k);
+    for (int k = 0; k < 8; ++k) x[k] = mp_max<T>(x[k] + a, y + (T)k);
   }
-  long long s = 0;
+  T s = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) s ^= x[k];
-  if (s == 0x5a5a5a5a5a5a5aLL) out[0] = s;
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == (T)12345) out[0] = (long long)s;
 }
 
-cudaError_t launch_maxplus_bench(long long* out, int grid, int iters, cudaStream_t st) {
-  maxplus_bench_kernel<<<grid, 256, 0, st>>>(out, iters, 3, 1LL << 40);
+// kind 0: int64, 1: FP64 (exact integers), 2: int32
+cudaError_t launch_maxplus_bench(int kind, long long* out, int grid, int iters, cudaStream_t st) {
+  if (kind == 1)
+    maxplus_bench_kernel<double><<<grid, 256, 0, st>>>(out, iters, 3.0, 1099511627776.0);
+  else if (kind == 2)
+    maxplus_bench_kernel<int><<<grid, 256, 0, st>>>(out, iters, 3, 1 << 20);
+  else
+    maxplus_bench_kernel<long long><<<grid, 256, 0, st>>>(out, iters, 3, 1LL << 40);
   return cudaGetLastError();
 }
 

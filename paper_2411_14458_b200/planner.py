@@ -84,6 +84,16 @@ def load_library(path: str = LIB_PATH):
         "gpb_fetch_row_cycles": (C.c_int, [C.c_void_p, P(C.c_int64), C.c_int64]),
         "gpb_bucket_infos": (C.c_int, [C.c_void_p, P(abi.BucketInfo), C.c_int32,
                                        P(C.c_int32)]),
+        "gpb_group_create": (C.c_void_p, [C.c_int32, P(C.c_int32)]),
+        "gpb_group_destroy": (None, [C.c_void_p]),
+        "gpb_group_last_error": (C.c_char_p, [C.c_void_p]),
+        "gpb_group_size": (C.c_int32, [C.c_void_p]),
+        "gpb_group_load": (C.c_int, [C.c_void_p, P(abi.Topology), C.c_int32, P(abi.Scenario),
+                                     C.c_int32, P(C.c_int64)]),
+        "gpb_group_evaluate": (C.c_int, [C.c_void_p]),
+        "gpb_group_fetch_rows": (C.c_int, [C.c_void_p, P(abi.Row), C.c_int64]),
+        "gpb_group_fetch_scenarios": (C.c_int, [C.c_void_p, P(abi.ScenarioResult), C.c_int32]),
+        "gpb_group_fetch_best": (C.c_int, [C.c_void_p, P(abi.Best)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -100,7 +110,9 @@ def exported_symbols():
             "gpb_synthetic_requests", "gpb_get_timing", "gpb_microbench", "gpb_set_stream",
             "gpb_copy_best", "gpb_set_profile", "gpb_fetch_row_cycles",
             "gpb_set_allreduce_tail", "gpb_timeline_arrays", "gpb_bucket_infos",
-            "gpb_set_bucket_timing"]
+            "gpb_set_bucket_timing", "gpb_group_create", "gpb_group_destroy",
+            "gpb_group_last_error", "gpb_group_size", "gpb_group_load", "gpb_group_evaluate",
+            "gpb_group_fetch_rows", "gpb_group_fetch_scenarios", "gpb_group_fetch_best"]
 
 
 @dataclass
@@ -254,6 +266,70 @@ class Planner:
         self._check(self.lib.gpb_pack_prefills(self.ctx, rows_arr, len(rows), req_arr, n_req,
                                                C.byref(pm), horizon_ns, summ, pl))
         return list(summ[: len(rows)]), pl
+
+
+class PlannerGroup:
+    """One plan space sharded over several devices of one box (gpb_group_*):
+    cost-balanced whole-scenario shards, one host thread per device, the
+    per-device winners all-gathered over NCCL. Results are in the order of
+    the whole space, identical to a single-device Planner."""
+
+    def __init__(self, devices=None):
+        self.lib = load_library()
+        devs = list(devices) if devices else []
+        arr = (C.c_int32 * max(1, len(devs)))(*devs)
+        self.g = self.lib.gpb_group_create(len(devs), arr if devs else None)
+        if not self.g:
+            raise GeopipeError(f"gpb_group_create({devs or 'all'}) failed")
+        self.n_rows = 0
+        self.n_scen = 0
+
+    def size(self) -> int:
+        return self.lib.gpb_group_size(self.g)
+
+    def close(self):
+        if self.g:
+            self.lib.gpb_group_destroy(self.g)
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int):
+        if rc != abi.GPB_OK:
+            msg = self.lib.gpb_group_last_error(self.g).decode()
+            raise _ERRS.get(rc, GeopipeError)(msg)
+
+    def load(self, topos, scens) -> int:
+        if not isinstance(topos, C.Array):
+            topos = abi.array(abi.Topology, list(topos))
+        scen_arr = scens if isinstance(scens, C.Array) else abi.array(abi.Scenario, list(scens))
+        n = C.c_int64()
+        self._check(self.lib.gpb_group_load(self.g, topos, len(topos), scen_arr, len(scens),
+                                            C.byref(n)))
+        self.n_rows, self.n_scen = n.value, len(scens)
+        return n.value
+
+    def evaluate(self):
+        self._check(self.lib.gpb_group_evaluate(self.g))
+
+    def rows(self):
+        out = (abi.Row * max(1, self.n_rows))()
+        self._check(self.lib.gpb_group_fetch_rows(self.g, out, self.n_rows))
+        return out
+
+    def scenario_results(self):
+        out = (abi.ScenarioResult * max(1, self.n_scen))()
+        self._check(self.lib.gpb_group_fetch_scenarios(self.g, out, self.n_scen))
+        return out
+
+    def best(self) -> abi.Best:
+        b = abi.Best()
+        self._check(self.lib.gpb_group_fetch_best(self.g, C.byref(b)))
+        return b
 
 
 def synthetic_requests(count: int, seed: int, horizon_ms: float, pm=None):

@@ -1,0 +1,117 @@
+"""GPU parity for BubbleTea at BASELINE config 4's shape (the bench's packing
+workload): the config-3 plan space (10^6 rows, Llama-3.1 405B over 5 DCs) is
+evaluated on the GPU, its top-1000 feasible plans by (throughput desc, row
+asc) are taken, and one synthetic trace (synthetic_requests(10^6, seed 42,
+horizon = the largest makespan of the 1000), bubbletea.cpp:269-284) is
+packed FCFS into each plan's bubbles (schedule_prefills,
+bubbletea.cpp:132-222).
+
+* test_config4_golden: the 2*10^4-request prefix of that trace on six of the
+  plans (all four policies, D = 50 / 66 / 100 / 200: the deepest pruning
+  paths — room-bound caps, the failure memo at minimum arrival, zero-layer
+  stage runs for D > inference_layers), bit-exact against fixtures frozen
+  from the reference's own schedule_prefills (oracle/_ref) by
+  tests/golden/make_config4_golden.py: accepted / rejected counts, the
+  placement hash, utilization before / after, and a digest of every
+  request's (accepted, pipeline, start_ns, ttft) outcome. The reference needs
+  1-4 h per plan for this prefix (its search is quadratic in the prefix), so
+  it is not rerun here; the top-1000 list itself is re-derived on the GPU and
+  must equal the frozen one.
+* test_config4_live_prefix: ten more of the top plans (largest D first) on a
+  10^3-request prefix, against the reference run live on the host.
+"""
+from concurrent.futures import ThreadPoolExecutor
+import json
+import os
+import struct
+
+import pytest
+
+from paper_2411_14458_b200 import abi, workloads
+from paper_2411_14458_b200.planner import synthetic_requests
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "config4_pack.json")
+TOP = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "config4_top.json")
+
+
+def _digest(pl):
+    h = 1469598103934665603
+    for p in pl:
+        for v in (p.accepted, p.pipeline & 0xffffffff, p.start_ns & 0xffffffffffffffff,
+                  struct.unpack("<Q", struct.pack("<d", p.ttft_overhead_ms))[0]):
+            for i in range(8):
+                h ^= (v >> (8 * i)) & 0xff
+                h = (h * 1099511628211) & 0xffffffffffffffff
+    return h
+
+
+@pytest.fixture(scope="module")
+def config3_top(planner):
+    topos, scens = workloads.config3(1_000_000, seed=2)
+    tarr, sarr = abi.array(abi.Topology, topos), abi.array(abi.Scenario, scens)
+    n = planner.load(tarr, sarr)
+    planner.evaluate()
+    rows = planner.rows()
+    feas = sorted(((r.throughput, i) for i, r in enumerate(rows[:n]) if r.feasible == 1),
+                  key=lambda x: (-x[0], x[1]))
+    top = [i for _, i in feas[:1000]]
+    info = [(i, rows[i].scenario, rows[i].d, rows[i].throughput, rows[i].makespan_ns)
+            for i in top]
+    return tarr, sarr, info
+
+
+def test_config4_golden(planner, config3_top):
+    tarr, sarr, info = config3_top
+    doc = json.load(open(GOLDEN))
+    # the top-1000 list (row, scenario, d, throughput) equals the frozen one
+    assert [[r, s, d, t.hex()] for r, s, d, t, _ in info] == doc["top"]
+    assert json.load(open(TOP))["top"] == doc["top"]
+    hmax = max(x[4] for x in info) / 1e6
+    assert hmax.hex() == doc["trace"]["horizon_ms"]
+    pm = abi.PrefillModel.default()
+    reqs = synthetic_requests(doc["trace"]["count"], doc["trace"]["seed"], hmax, pm)
+    n = doc["trace"]["prefix"]
+    assert n >= 20_000
+    prefix = (abi.Request * n).from_buffer_copy(reqs, 0)
+    plans = doc["plans"]
+    assert {p["policy"] for p in plans} == {"gpipe", "1f1b", "varuna", "atlas"}
+    assert max(p["d"] for p in plans) == 200
+    summ, pl = planner.pack_prefills([p["row"] for p in plans], prefix, pm, placements=True)
+    for k, p in enumerate(plans):
+        s = summ[k]
+        got = (s.accepted, s.rejected, s.horizon_ns, s.placement_hash,
+               s.utilization_before.hex(), s.utilization_after.hex(),
+               _digest(pl[k * n:(k + 1) * n]))
+        want = (p["accepted"], p["rejected"], p["horizon_ns"], p["placement_hash"],
+                p["utilization_before"], p["utilization_after"], p["placement_digest"])
+        assert got == want, (p["rank"], p["d"], p["policy"], got, want)
+
+
+def test_config4_live_prefix(planner, checker, config3_top):
+    tarr, sarr, info = config3_top
+    hmax = max(x[4] for x in info) / 1e6
+    pm = abi.PrefillModel.default()
+    n = 1000
+    reqs = synthetic_requests(1_000_000, 42, hmax, pm)
+    prefix = (abi.Request * n).from_buffer_copy(reqs, 0)
+    # the largest-D plans first (zero-layer stages), then the best ones
+    by_d = sorted(range(len(info)), key=lambda k: (-info[k][2], k))
+    ranks = sorted(set(by_d[:6] + [0, 1, 2, 3]))
+    plans = [info[k] for k in ranks]
+    summ, pl = planner.pack_prefills([x[0] for x in plans], prefix, pm, placements=True)
+
+    def ref(x):
+        return checker.pack(tarr, sarr[x[1]], x[2], list(prefix), pm)
+
+    with ThreadPoolExecutor(max_workers=len(plans)) as ex:
+        want = list(ex.map(ref, plans))
+    for k, (x, (ws, wpl)) in enumerate(zip(plans, want)):
+        s = summ[k]
+        assert (s.accepted, s.rejected, s.placement_hash, s.utilization_before,
+                s.utilization_after) == (ws.accepted, ws.rejected, ws.placement_hash,
+                                         ws.utilization_before, ws.utilization_after), x
+        for a, b in zip(pl[k * n:(k + 1) * n], wpl):
+            assert (a.accepted, a.pipeline, a.start_ns, a.ttft_overhead_ms) == \
+                (b.accepted, b.pipeline, b.start_ns, b.ttft_overhead_ms), x

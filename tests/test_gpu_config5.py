@@ -49,3 +49,48 @@ def test_grouped_rows_bit_exact(planner, checker, monkeypatch):
     scens = abi.array(abi.Scenario, scens)
     assert sum(1 for s in scens if -(-s.num_layers // s.layers_per_partition) <= 8) > 50
     assert _compare_space(planner, checker, bindings.port(), topos, scens) > 1500
+
+
+def test_atlas_seq_rows_bit_exact(planner, checker, monkeypatch):
+    """Large spaces run ATLAS rows of shallow pipelines (S <= 16) one per
+    thread (atlas_seq_kernel); force it on small spaces — config-5 shapes,
+    the unit12 KATs with memory caps, random caps/latencies — and check every
+    row against the reference (select() + report() on run())."""
+    import random
+    from oracle import bindings
+    from tests import fixtures
+    monkeypatch.setenv("GPB_GROUP_FLUSH_MIN_ROWS", "0")
+    monkeypatch.setenv("GPB_ATLAS_SEQ", "2")
+    for ml, ms in ((1, 89.0), (2, 67.0), (6, 36.0), (0, 36.0)):
+        topos, sc = fixtures.unit12(policy="atlas", mem_limit=ml)
+        assert planner.select(topos, sc).rows[0].pp_time_ms == ms
+    topos, scens = workloads.config5(3000, seed=31, max_rows_per_scenario=3)
+    scens = [s for s in scens if s.policy == 3
+             and -(-s.num_layers // s.layers_per_partition) <= 16]
+    assert len(scens) > 100
+    topos = abi.array(abi.Topology, topos)
+    assert _compare_space(planner, checker, bindings.port(), topos,
+                          abi.array(abi.Scenario, scens)) > 300
+    rng = random.Random(8)
+    topos, scens = [], []
+    for _ in range(120):
+        n_dc = rng.randint(2, 6)
+        counts = [rng.choice([64, 128, 256]) for _ in range(n_dc)]
+        lat = [[0.0] * n_dc for _ in range(n_dc)]
+        for i in range(n_dc):
+            for j in range(i + 1, n_dc):
+                lat[i][j] = lat[j][i] = rng.choice([0.0, 5.0, 20.0, 80.0])
+        topos.append(abi.make_topology(counts, cap_gbps=rng.choice([1.0, 5.0, 25.0]),
+                                       intra_gbps=100.0, latency=lat))
+        S = rng.randint(2, 16)
+        scens.append(abi.make_scenario(
+            topology=len(topos) - 1, policy="atlas", num_layers=S,
+            num_microbatches=rng.choice([1, 3, 8, 33, 64]),
+            hidden=rng.choice([512, 4096]), seq_len=rng.choice([512, 4096]),
+            fwd_ms=rng.uniform(0.5, 20.0), bwd_ms=rng.uniform(1.0, 40.0),
+            recompute_ms=rng.uniform(0.0, 10.0), C=rng.choice([1, 2, 3, 4, 6]),
+            recompute=rng.random() < 0.5, multi_conn=rng.random() < 0.5,
+            mem_limit=rng.choice([0, 1, 2, 3, S]), d_max=rng.choice([1, 2]),
+            dc_order=list(range(n_dc))))
+    assert _compare_space(planner, checker, bindings.port(), abi.array(abi.Topology, topos),
+                          abi.array(abi.Scenario, scens)) >= 120

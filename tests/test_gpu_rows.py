@@ -171,3 +171,23 @@ def test_reload_same_shapes_and_stream_switch(planner, checker):
         r0 = planner.scenario_results()[i].first_row
         for a, b in zip(rows[r0:r0 + len(ref_rows)], ref_rows):
             assert _row_key(a) == _row_key(b)
+
+
+def test_graph_mode_reloads(planner, checker, monkeypatch):
+    """GPB_GRAPH=1 replays the evaluate launch sequence as a CUDA graph; a
+    reload (same bucket shapes with other values, a different scenario split,
+    another space) must re-capture it: every row stays bit-exact."""
+    import ctypes
+    monkeypatch.setenv("GPB_GRAPH", "1")
+    topos, scens = random_space(4321, 120, wide=False)
+    assert _compare_space(planner, checker, None, topos, scens) > 120
+    scens2 = abi.array(abi.Scenario, [type(s).from_buffer_copy(s) for s in scens])
+    for s in scens2:
+        s.fwd_ms, s.bwd_ms = s.fwd_ms * 1.25, s.bwd_ms * 0.8
+    assert _compare_space(planner, checker, None, topos, scens2) > 120
+    # same rows split over scenarios differently (d_max moved between two)
+    scens3 = abi.array(abi.Scenario, [type(s).from_buffer_copy(s) for s in scens])
+    assert ctypes.sizeof(scens3[0]) == ctypes.sizeof(abi.Scenario)
+    assert _compare_space(planner, checker, None, topos, scens3[::-1]) > 120
+    topos4, scens4 = random_space(99, 80, wide=True)
+    assert _compare_space(planner, checker, None, topos4, scens4) > 80

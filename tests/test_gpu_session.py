@@ -126,3 +126,20 @@ def test_error_codes_match(libs, tmp_path):
         s.load_config_text(bad.encode())
         assert s.run_simulate(str(tmp_path / "d").encode()) == 3
         s.close()
+
+
+@pytest.mark.parametrize("cfg,cmd", [(c, m) for c in CONFIGS if "whatif" in c or "select" in c
+                                     for m in ("whatif", "select_dc") if "whatif" in c or
+                                     m == "select_dc"])
+def test_sharded_selection_byte_identical(libs, tmp_path, monkeypatch, cfg, cmd):
+    """gp_run_whatif / gp_run_select_dc with the space sharded over a device
+    group (GEOPIPE_DEVICES; two contexts on device 0 here, every GPU on a
+    multi-GPU box) write the reference's bytes."""
+    ref_so, ours = libs
+    monkeypatch.setenv("GEOPIPE_DEVICES", "0,0")
+    a, b = tmp_path / "ref", tmp_path / "ours"
+    ra = _run(ref_so, cfg, cmd, str(a))
+    rb = _run(ours, cfg, cmd, str(b))
+    assert ra[:2] == rb[:2], (ra, rb)
+    fa, fb = _files(a), _files(b)
+    assert fa.keys() == fb.keys() and all(fa[k] == fb[k] for k in fa)

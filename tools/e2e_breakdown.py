@@ -1,5 +1,8 @@
 """Where the e2e step goes: gpb_load (host flatten + H2D), gpb_evaluate,
-gpb_fetch_rows (D2H) wall times on the bench workload."""
+gpb_fetch_rows (D2H) wall times on a BASELINE workload.
+
+    python tools/e2e_breakdown.py [config2|config3|config5] [K=20]
+"""
 import sys
 import time
 
@@ -7,7 +10,9 @@ sys.path.insert(0, ".")
 from paper_2411_14458_b200 import abi, workloads  # noqa: E402
 from paper_2411_14458_b200.planner import Planner  # noqa: E402
 
-topos, scens = workloads.config2()
+cfg = sys.argv[1] if len(sys.argv) > 1 else "config2"
+K = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+topos, scens = getattr(workloads, cfg)()
 tarr = abi.array(abi.Topology, topos)
 sarr = abi.array(abi.Scenario, scens)
 p = Planner(0)
@@ -20,7 +25,6 @@ for _ in range(3):
     p.evaluate()
     p.lib.gpb_fetch_rows(p.ctx, out, n)
 tl = te = tf = 0.0
-K = 20
 for _ in range(K):
     t0 = time.perf_counter()
     p.load(tarr, sarr)
