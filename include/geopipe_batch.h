@@ -243,7 +243,27 @@ int gpb_pack_prefills(gpb_ctx* ctx, const int64_t* rows, int32_t n_rows_sel,
  * behind gpb_bubbles and gpb_pack_prefills. Default off. */
 int gpb_set_allreduce_tail(gpb_ctx* ctx, int32_t enable);
 
-/* Deterministic request sources on the host (bubbletea.cpp:240-284). */
+/* saturating_requests (bubbletea.cpp:240-267) on the device: every prefill
+ * pipeline's head GPU's bubbles of one row's timeline (horizon_ns <= 0 =>
+ * makespan) filled with back-to-back requests of the largest fitting token
+ * count, in build_prefill_pipelines order. Writes the requests when
+ * cap >= *n_out (the full count). */
+int gpb_saturating_requests(gpb_ctx* ctx, int64_t row, const gpb_prefill_model* pm,
+                            int64_t horizon_ns, gpb_request* out, int64_t cap,
+                            int64_t* n_out);
+
+/* On-device structural check of one row's iteration timeline (cell 0), the
+ * reference's validate_timeline (tests/support/validate.h:77-256): *check =
+ * 0 valid, 1 incomplete, 2 overlapping tasks on a GPU, 3 overlapping
+ * transfers on a link lane, 4 forward before its activation arrives, 5
+ * recompute/backward before its gradient (or forward) arrives, 6 makespan
+ * is not the last task end; *where = (pipeline << 48 | stage << 32 |
+ * microbatch) of the first failure. fe / ps (nullable) replace the device's
+ * own timeline with caller arrays in gpb_timeline_arrays' layout. */
+int gpb_validate_timeline(gpb_ctx* ctx, int64_t row, const int64_t* fe, const int64_t* ps,
+                          int32_t* check, int64_t* where);
+
+/* Deterministic request sources on the host (bubbletea.cpp:269-284). */
 int gpb_synthetic_requests(int32_t count, uint32_t seed, double horizon_ms,
                            const gpb_prefill_model* pm, gpb_request* out);
 

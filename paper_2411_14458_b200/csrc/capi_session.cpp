@@ -1077,48 +1077,7 @@ std::vector<Request> parse_requests_csv(const std::string& text) {  // config.cp
   return out;
 }
 
-long long prefill_dur_ns(const gpb_prefill_model& pm, int tokens) {
-  return ms_to_ns(pm.saturation_ms * static_cast<double>(tokens) / static_cast<double>(pm.max_tokens));
-}
 
-// saturating_requests (bubbletea.cpp:240-267) from the host timeline.
-std::vector<Request> saturating(const Timeline& t, const PlanInfo& plan, const gpb_prefill_model& pm,
-                                long long horizon) {
-  std::map<int, std::vector<std::pair<long long, long long>>> busy;
-  for (const Task& x : t.tasks) {
-    const long long lo = std::max(x.start, 0LL), hi = std::min(x.end, horizon);
-    if (lo >= hi) continue;
-    busy[x.gpu].push_back({lo, hi});
-  }
-  for (auto& kv : busy) std::sort(kv.second.begin(), kv.second.end(),
-                                  [](const auto& a, const auto& b) { return a.first < b.first; });
-  std::vector<Request> out;
-  int next_id = 0;
-  for (int pipe = 0; pipe < plan.C; ++pipe)
-    for (int st = 0; st < plan.S; ++st) {
-      const int gpu = plan.gpu[((size_t)0 * plan.C + pipe) * plan.S + st];
-      std::vector<std::pair<long long, long long>> gaps;
-      long long cursor = 0;
-      for (const auto& sp : busy[gpu]) {
-        if (sp.first > cursor) gaps.push_back({cursor, sp.first});
-        cursor = std::max(cursor, sp.second);
-      }
-      if (cursor < horizon) gaps.push_back({cursor, horizon});
-      for (const auto& g : gaps) {
-        long long cur = g.first;
-        while (cur < g.second) {
-          const double gap_ms = ns_to_ms(g.second - cur);
-          int tokens = static_cast<int>(gap_ms * pm.max_tokens / pm.saturation_ms);
-          tokens = std::min(tokens, pm.max_tokens);
-          while (tokens >= 1 && cur + prefill_dur_ns(pm, tokens) > g.second) tokens -= 1;
-          if (tokens < 1) break;
-          out.push_back({next_id++, ns_to_ms(cur), tokens});
-          cur += prefill_dur_ns(pm, tokens);
-        }
-      }
-    }
-  return out;
-}
 
 // ------------------------------------------------------------ runners
 
@@ -1179,23 +1138,10 @@ void run_bubbletea(Session& se, const std::string& out_dir) {
   Timeline t = simulate(se, c, c.policy, plan);
   const long long horizon = c.horizon_ms ? ms_to_ns(*c.horizon_ms) : t.makespan;
   const gpb_prefill_model& pm = c.prefill;
-  std::vector<Request> reqs;
-  if (c.requests_csv) {
-    reqs = parse_requests_csv(read_text_file(*c.requests_csv));
-  } else if (c.synthetic_count) {
-    std::vector<gpb_request> g(std::max(1, *c.synthetic_count));
-    if (gpb_synthetic_requests(*c.synthetic_count, c.seed, ns_to_ms(horizon), &pm, g.data()) != GPB_OK)
-      throw ConfigError("prefill.synthetic", "invalid");
-    for (int i = 0; i < *c.synthetic_count; ++i) reqs.push_back({g[i].id, g[i].arrival_ms, g[i].tokens});
-  } else if (c.saturating) {
-    reqs = saturating(t, plan, pm, horizon);
-  }
-  // pack on the device (the plan space of the simulate call is still loaded)
+  // the simulate plan on the device (the reference-policy run may have
+  // replaced it): saturating requests and the packing run on its timeline
   gpb_ctx* ctx = se.device();
-  std::vector<gpb_request> greq(reqs.size());
-  for (size_t i = 0; i < reqs.size(); ++i) greq[i] = {reqs[i].id, reqs[i].tokens, reqs[i].arrival_ms};
   {
-    // re-load the simulate plan (the reference-policy run may have replaced it)
     gpb_topology gt = to_gpb(c.topo);
     gpb_scenario s = base_scenario(c);
     s.policy = policy_code(c.policy);
@@ -1208,6 +1154,27 @@ void run_bubbletea(Session& se, const std::string& out_dir) {
     se.check(gpb_evaluate(ctx, 1));
   }
   const int64_t row = c.dp_cells - 1;
+  std::vector<Request> reqs;
+  if (c.requests_csv) {
+    reqs = parse_requests_csv(read_text_file(*c.requests_csv));
+  } else if (c.synthetic_count) {
+    std::vector<gpb_request> g(std::max(1, *c.synthetic_count));
+    if (gpb_synthetic_requests(*c.synthetic_count, c.seed, ns_to_ms(horizon), &pm, g.data()) != GPB_OK)
+      throw ConfigError("prefill.synthetic", "invalid");
+    for (int i = 0; i < *c.synthetic_count; ++i) reqs.push_back({g[i].id, g[i].arrival_ms, g[i].tokens});
+  } else if (c.saturating) {
+    // saturating_requests (bubbletea.cpp:240-267) on the device timeline
+    se.check(gpb_set_allreduce_tail(ctx, c.with_allreduce ? 1 : 0));
+    int64_t n = 0;
+    int rc = gpb_saturating_requests(ctx, row, &pm, horizon, nullptr, 0, &n);
+    std::vector<gpb_request> g(std::max<int64_t>(1, n));
+    if (rc == GPB_OK) rc = gpb_saturating_requests(ctx, row, &pm, horizon, g.data(), n, &n);
+    gpb_set_allreduce_tail(ctx, 0);
+    se.check(rc);
+    for (int64_t i = 0; i < n; ++i) reqs.push_back({g[i].id, g[i].arrival_ms, g[i].tokens});
+  }
+  std::vector<gpb_request> greq(reqs.size());
+  for (size_t i = 0; i < reqs.size(); ++i) greq[i] = {reqs[i].id, reqs[i].tokens, reqs[i].arrival_ms};
   gpb_pack_summary sum;
   std::vector<gpb_placement> pl(std::max<size_t>(1, reqs.size()));
   se.check(gpb_set_allreduce_tail(ctx, c.with_allreduce ? 1 : 0));

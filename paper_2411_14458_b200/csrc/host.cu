@@ -439,7 +439,8 @@ static bool same_shapes(const std::vector<Bucket>& a, const std::vector<Bucket>&
     if (x.policy != y.policy || x.B != y.B || x.offset != y.offset || x.count != y.count ||
         x.max_m != y.max_m || x.max_cs != y.max_cs || x.max_cm != y.max_cm ||
         x.max_csm != y.max_csm || x.max_c != y.max_c || x.max_s != y.max_s ||
-        x.max_nw != y.max_nw || x.heavy != y.heavy || x.gw != y.gw)
+        x.max_nw != y.max_nw || x.heavy != y.heavy || x.gw != y.gw ||
+        x.max_slice != y.max_slice)
       return false;
   }
   return true;
@@ -496,11 +497,14 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   // =2 also takes heavy rows (tests)
   const int seq_mode = atlas_seq_mode();
   auto seq_ok = [&](const DevScen& d, bool heavy) {
-    return seq_mode > 0 && n_rows >= group_min && d.S <= 16 && (!heavy || seq_mode == 2) &&
-           atlas_seq_slice(d.C, d.S, d.M, d.n_order - 1) <= kSeqMaxSlice;
+    return seq_mode > 0 && n_rows >= group_min && d.S <= 16 && d.C <= 8 &&
+           (!heavy || seq_mode == 2) &&
+           atlas_seq_slice(d.C, d.S, d.M, d.n_order - 1, d.mem_limit) <= kSeqMaxSlice;
   };
   auto gw_of = [&](const DevScen& d, bool heavy) {
-    if (d.policy == GPB_ATLAS) return seq_ok(d, heavy) ? 1 : 32;
+    // ATLAS: 32 = one warp per row, 4 / 8 / 16 = one thread per row with
+    // stage loops unrolled to that bound (atlas_seq_kernel<SMAX>)
+    if (d.policy == GPB_ATLAS) return seq_ok(d, heavy) ? (d.S <= 4 ? 4 : d.S <= 8 ? 8 : 16) : 32;
     if (kNoGroupFlush || n_rows < group_min) return 32;
     const int gw = d.S <= 8 ? 8 : (d.S <= 16 ? 16 : 32);
     // the per-row last-stage buffer (M entries per row) must fit the block
@@ -510,7 +514,7 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   for (int i = 0; i < n_scen; ++i) {
     int heavy = ds[i].policy == GPB_ATLAS && cost(i) >= 0.3 * max_atlas;
     const int gw = gw_of(ds[i], heavy != 0);
-    if (gw == 1) heavy = 0;
+    if (ds[i].policy == GPB_ATLAS && gw < 32) heavy = 0;
     by_key[{ds[i].policy, (ds[i].S + 31) / 32, heavy, gw}].push_back(i);
   }
   std::vector<int32_t> bscen;
@@ -538,6 +542,9 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
       b.max_c = std::max(b.max_c, ds[i].C);
       b.max_s = std::max(b.max_s, ds[i].S);
       b.max_nw = std::max(b.max_nw, ds[i].n_order - 1);
+      if (b.policy == GPB_ATLAS && b.gw < 32)
+        b.max_slice = std::max(b.max_slice, atlas_seq_slice(ds[i].C, ds[i].S, ds[i].M,
+                                                            ds[i].n_order - 1, ds[i].mem_limit));
     }
     b.count = (int32_t)(n_work - b.offset);
     b.scen_off = (int32_t)bscen.size();
@@ -703,7 +710,8 @@ static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
       a.scratch_per_warp = P.scratch_per_warp;
       a.scratch_big_off = P.scratch_big_off;
       a.scratch = P.scratch_per_warp > 0 ? (long long*)c.b_scratch.ptr + c.scr_off[bi] : nullptr;
-      e = b.gw == 1 ? launch_atlas_seq(a, P.grid, ss) : launch_atlas(b.B, a, P.grid, P.wpc, ss);
+      e = b.gw < 32 ? launch_atlas_seq(b.gw, a, P.grid, ss)
+                    : launch_atlas(b.B, a, P.grid, P.wpc, ss);
     }
     if (e != cudaSuccess) return c.cuda_fail(e, "eval launch");
     if (bt) rec(c.bucket_ev_end[bi], ss);
@@ -776,11 +784,11 @@ static int prepare_evaluate(Ctx& c) {
   for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
     const Bucket& b = c.buckets[bi];
     if (b.policy != GPB_ATLAS || b.count == 0) continue;
-    if (b.gw == 1) {  // one thread per row: a [element][lane] slice per thread
+    if (b.gw < 32) {  // one thread per row: a [element][lane] slice per thread
       AtlasPlan& P = c.aplan[bi];
-      const long long slice = atlas_seq_slice(b.max_c, b.max_s, b.max_m, b.max_nw);
+      const long long slice = b.max_slice;
       P.wpc = kEvalThreads / 32;
-      const long long per_sm = std::max(1, atlas_seq_blocks_per_sm());
+      const long long per_sm = std::max(1, atlas_seq_blocks_per_sm(b.gw));
       long long grid = std::min<long long>((long long)c.num_sms * per_sm,
                                            (b.count + kEvalThreads - 1) / kEvalThreads);
       // scratch bound: 12 GiB per bucket (rows beyond the resident ones reuse it)

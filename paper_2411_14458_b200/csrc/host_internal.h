@@ -32,6 +32,7 @@ struct Bucket {
   int max_cm = 0;
   long long max_csm = 0;
   int max_c = 0, max_s = 0, max_nw = 0;
+  long long max_slice = 0;  // atlas_seq buckets: per-thread scratch slice (int64)
   double est = 0;   // estimated bucket makespan (same units as cost)
   double cost = 0;  // estimated cost of the bucket's heaviest row
   int stream = 0;   // side stream it ran on
@@ -101,6 +102,7 @@ struct Ctx {
   cudaStream_t pack_side = nullptr;    // pack: the heavy plans' launch
   cudaEvent_t pack_fork = nullptr, pack_join = nullptr;
   bool pack_allreduce = false;  // include the all-reduce tail in timelines
+  bool pack_warm = false;       // pack kernels launched once (module loaded)
   // last build_timelines() outputs (device pointers into the buffers above)
   long long *tl_glo = nullptr, *tl_ghi = nullptr, *tl_gsum = nullptr, *tl_hz = nullptr;
   unsigned char* tl_gfl = nullptr;

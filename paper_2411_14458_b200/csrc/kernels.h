@@ -60,9 +60,9 @@ cudaError_t launch_atlas(int B, const EvalArgs& a, int grid, int wpc, cudaStream
 int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem);
 // one thread per ATLAS row (bulk of large spaces); scratch_per_warp = 32 x
 // the per-thread slice (int64 elements) for rows up to (C, S, M, nw)
-long long atlas_seq_slice(int C, int S, int M, int nw);
-int atlas_seq_blocks_per_sm();
-cudaError_t launch_atlas_seq(const EvalArgs& a, int grid, cudaStream_t st);
+long long atlas_seq_slice(int C, int S, int M, int nw, int L);
+int atlas_seq_blocks_per_sm(int smax);
+cudaError_t launch_atlas_seq(int smax, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_select(const SelectArgs& a, int grid, cudaStream_t st);
 // select_kernel alone (per bucket) / the final reduction of the block bests
 cudaError_t launch_select_part(const SelectArgs& a, int grid, cudaStream_t st);

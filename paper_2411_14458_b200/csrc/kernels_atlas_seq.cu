@@ -9,12 +9,18 @@
 // its own row with the reference's sequential recurrences, so 32 rows share
 // one instruction stream.
 //
-// The state of a row lives in a per-thread slice of global scratch laid out
-// [element][lane] per warp (lanes at the same step touch one 256-byte line):
+// The state of a row lives in a per-thread slice of global scratch:
 //   GF[C][S]   gpu_free        DR[C][S]  drained counts
-//   FDL[C][M]  last-stage forward ends (written once per forward)
-//   GA[C][S][M] gradient arrivals at stage s (pair m's arrival exists once
-//              stage s+1 has drained pair m: DR[p][s+1] > m)
+//   FDL[C][R]  last-stage forward ends, ring of R slots
+//   GA[C][S][R] gradient arrivals at stage s, ring of R slots (pair m's
+//              arrival exists once stage s+1 has drained pair m)
+// A pair is "in flight" at stage s between its producer's commit (stage s+1,
+// or the forward at S-1) and its own drain. The memory cap keeps at most
+// L = mem_limit pairs in flight per stage: after every admission no stage
+// is blocked (m - drained[s] < L), a cascade drains a stage only after the
+// stage above, and after the last admission at most L pairs remain per
+// stage for the drain phase. So rings of R = 2^ceil(log2(min(L, M))) slots
+// indexed m & (R-1) hold every live value (the reference keeps all M).
 //   per WAN link w: MF / MB merged static forward / gradient reservation
 //   starts of the pipelines before the current one (C*M each), OF / OB the
 //   current pipeline's own starts (M each).
@@ -40,25 +46,39 @@ namespace gpb {
 namespace {
 
 constexpr long long kNegInf = -(1LL << 60);
+constexpr int kSeqMaxC = 8;  // pipelines per cell (host-checked)
 
-// One thread's row state, interleaved with the other 31 lanes of its warp.
+// One thread's row state: a contiguous slice, so the streams a row walks
+// (its rings, list cursors, appends) stay within few cache lines. Lanes of a
+// warp diverge in shape and progress, so an [element][lane] interleave buys
+// no coalescing and costs a new line per element (measured: 43% L2 hits,
+// long-scoreboard bound).
 struct SeqMem {
-  long long* base;  // warp base + lane
-  __device__ __forceinline__ long long& at(long long k) const { return base[k * 32]; }
+  long long* base;
+  __device__ __forceinline__ long long& at(long long k) const { return base[k]; }
 };
+
+// ring slots for a row: the smallest power of two >= min(mem_limit, M)
+__host__ __device__ __forceinline__ int seq_ring(int L, int M) {
+  const int n = L < M ? L : M;
+  int r = 1;
+  while (r < n) r <<= 1;
+  return r;
+}
 
 struct SeqLayout {
   long long gf, dr, fdl, ga, links, per_link;
-  int C, S, M;
-  __device__ __forceinline__ void make(int C_, int S_, int M_) {
+  int C, S, M, R;
+  __device__ __forceinline__ void make(int C_, int S_, int M_, int R_) {
     C = C_;
     S = S_;
     M = M_;
+    R = R_;
     gf = 0;
     dr = gf + (long long)C * S;
     fdl = dr + (long long)C * S;
-    ga = fdl + (long long)C * M;
-    links = ga + (long long)C * S * M;
+    ga = fdl + (long long)C * R;
+    links = ga + (long long)C * S * R;
     per_link = 2LL * C * M + 2LL * M;
   }
   __device__ __forceinline__ long long mf(int w) const { return links + w * per_link; }
@@ -104,21 +124,33 @@ __device__ __forceinline__ void merge_into(const SeqMem& X, long long st, int ns
   }
 }
 
+// WAN link of boundary s -> s+1, or -1
+__device__ __forceinline__ int link_of(const Geom& g, int s) {
+  for (int b = 1; b < g.nb; ++b)
+    if (g.blk_first[b] == s + 1) return b - 1;
+  return -1;
+}
+
 }  // namespace
 
-// One ATLAS row on one thread; returns the makespan.
+// One ATLAS row on one thread; returns the makespan. SMAX >= S bounds the
+// stage loops, which are unrolled so the current pipeline's per-stage state
+// (gpu_free, drained counts, WAN links) stays in registers.
+template <int SMAX>
 __device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
   const int S = g.S, M = g.M, C = g.C;
   const long long f = g.fwd, dur = g.dur;
   SeqLayout Y;
-  Y.make(C, S, M);
+  const int R = seq_ring(L, M), RM = R - 1;
+  Y.make(C, S, M, R);
   const int nw = g.nb - 1;
-  auto link_after = [&](int s) -> int {  // WAN link of boundary s -> s+1
+  int lk[SMAX];  // WAN link of boundary s -> s+1, or -1
+#pragma unroll
+  for (int s = 0; s < SMAX; ++s) {
+    lk[s] = -1;
     for (int b = 1; b < g.nb; ++b)
-      if (g.blk_first[b] == s + 1) return b - 1;
-    return -1;
-  };
-  for (long long i = 0; i < 2LL * C * S; ++i) X.at(Y.gf + i) = 0;
+      if (g.blk_first[b] == s + 1 && s + 1 < S) lk[s] = b - 1;
+  }
   int nf[GPB_MAX_DC], nb_[GPB_MAX_DC], of_n[GPB_MAX_DC], ob_n[GPB_MAX_DC];
   for (int w = 0; w < nw; ++w) nf[w] = nb_[w] = of_n[w] = ob_n[w] = 0;
 
@@ -135,58 +167,66 @@ __device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
     }
     int cf[GPB_MAX_DC], cb[GPB_MAX_DC];
     for (int w = 0; w < nw; ++w) cf[w] = cb[w] = 0;
-    const long long gfp = Y.gf + (long long)p * S, drp = Y.dr + (long long)p * S;
+    long long gfr[SMAX];
+    int drr[SMAX];
+#pragma unroll
+    for (int s = 0; s < SMAX; ++s) {
+      gfr[s] = 0;
+      drr[s] = 0;
+    }
+    const long long fdlp = Y.fdl + (long long)p * R, gap = Y.ga + (long long)p * S * R;
     for (int m = 0; m < M; ++m) {
-      // memory-cap admission (:366-381): drain the deepest stage with a ready
-      // pair (atlas_drain_step, :321-346) while some stage is blocked
-      for (;;) {
-        bool blocked = false;
-        for (int s = 0; s < S; ++s)
-          if (m - (int)X.at(drp + s) >= L) {
-            blocked = true;
-            break;
-          }
-        if (!blocked) break;
-        bool drained = false;
-        for (int s = S - 1; s >= 0 && !drained; --s) {
-          const int mm = (int)X.at(drp + s);
-          if (mm >= M) continue;
-          // ready: forwarded (microbatches < m are) / gradient arrived
-          if (s == S - 1 ? mm >= m : (int)X.at(drp + s + 1) <= mm) continue;
-          const long long ready = s == S - 1
-                                      ? X.at(Y.fdl + (long long)p * M + mm)
-                                      : X.at(Y.ga + ((long long)p * S + s) * M + mm);
-          long long lo = imax(ready, X.at(gfp + s));
-          const int w = s > 0 ? link_after(s - 1) : -1;
-          long long t = lo;
-          if (w >= 0) {  // atlas_pair_start (:287-294) + reserve
-            const long long len = g.ser_pooled[w];
-            if (len > 0) {
+      // memory-cap admission (:366-381): the reference repeats
+      // atlas_drain_step (:321-346), "drain the deepest stage with a ready
+      // pair", while some stage is blocked (m - drained >= L). Draining a
+      // stage unblocks only itself and readies only the stage below, so the
+      // repetition is: every stage above the lowest blocked one s_min drains
+      // all its ready pairs (up to m-1), s_min drains to m-L+1; each
+      // gradient link has one writer stage, so stages run one after another.
+      int s_min = -1;
+#pragma unroll
+      for (int s = SMAX - 1; s >= 0; --s)
+        if (s < S && m - drr[s] >= L) s_min = s;
+      if (s_min >= 0) {
+#pragma unroll
+        for (int s = SMAX - 1; s >= 0; --s) {
+          if (s >= S || s < s_min) continue;
+          const int upto = s == s_min ? m - L + 1 : m;
+          const int w = s > 0 ? lk[s - 1] : -1;
+          const long long len = w >= 0 ? g.ser_pooled[w] : 0;
+          const long long wl = w >= 0 ? len + g.lat[w] : 0;
+          long long gv = gfr[s];
+          for (int mm = drr[s]; mm < upto; ++mm) {
+            const long long ready =
+                s == S - 1 ? X.at(fdlp + (mm & RM)) : X.at(gap + (long long)s * R + (mm & RM));
+            long long t = imax(ready, gv);
+            if (len > 0) {  // atlas_pair_start (:287-294) + reserve
               const long long own = ob_n[w] > 0 ? X.at(Y.ob(w) + ob_n[w] - 1) : kNegInf;
-              t = fit(X, Y.mb(w), nb_[w], cb[w], own, len, lo + dur) - dur;
+              t = fit(X, Y.mb(w), nb_[w], cb[w], own, len, t + dur) - dur;
               X.at(Y.ob(w) + ob_n[w]) = t + dur;
               ++ob_n[w];
             }
+            gv = t + dur;  // atlas_commit_pair (:298-317)
+            if (s > 0) X.at(gap + (long long)(s - 1) * R + (mm & RM)) = gv + wl;
           }
-          const long long e = t + dur;  // atlas_commit_pair (:298-317)
-          X.at(gfp + s) = imax(X.at(gfp + s), e);
-          if (s > 0)
-            X.at(Y.ga + ((long long)p * S + s - 1) * M + mm) =
-                w >= 0 ? e + g.ser_pooled[w] + g.lat[w] : e;
-          X.at(drp + s) = mm + 1;
-          drained = true;
+          if (upto > drr[s]) {
+            gfr[s] = gv;
+            drr[s] = upto;
+          }
         }
-        if (!drained) return -1;  // DeadlockError in the reference (unreachable)
       }
       // the chain: shift t0 until every WAN transfer fits at its compute end
-      long long t0 = X.at(gfp + 0);
+      // (:383-405), then commit (:407-430)
+      long long t0 = gfr[0];
       for (;;) {
         bool ok = true;
         long long cur = t0;
-        for (int s = 0; s < S; ++s) {
-          const long long e = imax(cur, X.at(gfp + s)) + f;
-          if (s + 1 < S) {
-            const int w = link_after(s);
+#pragma unroll
+        for (int s = 0; s < SMAX; ++s) {
+          if (s < S && ok) {
+            const long long e = imax(cur, gfr[s]) + f;
+            const int w = lk[s];
+            cur = e;
             if (w >= 0) {
               const long long len = g.ser_pooled[w];
               if (len > 0) {
@@ -195,36 +235,39 @@ __device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
                 if (slot != e) {
                   t0 += slot - e;
                   ok = false;
-                  break;
                 }
               }
               cur = e + len + g.lat[w];
-            } else {
-              cur = e;
             }
           }
         }
         if (ok) break;
       }
-      long long cur = t0;  // commit (:407-430)
-      for (int s = 0; s < S; ++s) {
-        const long long e = imax(cur, X.at(gfp + s)) + f;
-        X.at(gfp + s) = e;
-        if (s == S - 1) X.at(Y.fdl + (long long)p * M + m) = e;
-        if (s + 1 < S) {
-          const int w = link_after(s);
+      long long cur = t0;
+#pragma unroll
+      for (int s = 0; s < SMAX; ++s) {
+        if (s < S) {
+          const long long e = imax(cur, gfr[s]) + f;
+          gfr[s] = e;
+          cur = e;
+          const int w = lk[s];
           if (w >= 0) {
             if (g.ser_pooled[w] > 0) {
               X.at(Y.of(w) + of_n[w]) = e;
               ++of_n[w];
             }
             cur = e + g.ser_pooled[w] + g.lat[w];
-          } else {
-            cur = e;
           }
+          if (s == S - 1) X.at(fdlp + (m & RM)) = e;
         }
       }
     }
+#pragma unroll
+    for (int s = 0; s < SMAX; ++s)
+      if (s < S) {
+        X.at(Y.gf + (long long)p * S + s) = gfr[s];
+        X.at(Y.dr + (long long)p * S + s) = drr[s];
+      }
   }
   // the last pipeline's forced drains join the static gradient lists
   for (int w = 0; w < nw; ++w) {
@@ -235,17 +278,17 @@ __device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
   // ------------------------------------------- drain: stage by stage
   long long mk = 0;
   for (int s = S - 1; s >= 0; --s) {
-    const int w = s > 0 ? link_after(s - 1) : -1;
+    const int w = s > 0 ? link_of(g, s - 1) : -1;
     const long long len = w >= 0 ? g.ser_pooled[w] : 0;
     if (w < 0 || len <= 0) {  // no shared resource: e[m] = max(r[m], e[m-1]) + dur
       const long long wl2 = w >= 0 ? g.lat[w] : 0;  // len == 0 WAN stage: latency only
       for (int p = 0; p < C; ++p) {
         long long gfv = X.at(Y.gf + (long long)p * S + s);
         for (int m = (int)X.at(Y.dr + (long long)p * S + s); m < M; ++m) {
-          const long long r = s == S - 1 ? X.at(Y.fdl + (long long)p * M + m)
-                                         : X.at(Y.ga + ((long long)p * S + s) * M + m);
+          const long long r = s == S - 1 ? X.at(Y.fdl + (long long)p * R + (m & RM))
+                                         : X.at(Y.ga + ((long long)p * S + s) * R + (m & RM));
           gfv = imax(r, gfv) + dur;
-          if (s > 0) X.at(Y.ga + ((long long)p * S + s - 1) * M + m) = gfv + wl2;
+          if (s > 0) X.at(Y.ga + ((long long)p * S + s - 1) * R + (m & RM)) = gfv + wl2;
         }
         X.at(Y.gf + (long long)p * S + s) = gfv;
         mk = imax(mk, gfv);
@@ -255,15 +298,15 @@ __device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
     // WAN gradient link: greedy over the pipelines' next pairs
     const long long wl2 = len + g.lat[w];
     long long last = kNegInf;  // start of this stage's last committed transfer
-    long long cand[32];
-    int mq[32], cq[32];
+    long long cand[kSeqMaxC];
+    int mq[kSeqMaxC], cq[kSeqMaxC];
     for (int q = 0; q < C; ++q) {
       mq[q] = (int)X.at(Y.dr + (long long)q * S + s);
       cq[q] = 0;
       cand[q] = kInf64;
       if (mq[q] < M) {
-        const long long r = s == S - 1 ? X.at(Y.fdl + (long long)q * M + mq[q])
-                                       : X.at(Y.ga + ((long long)q * S + s) * M + mq[q]);
+        const long long r = s == S - 1 ? X.at(Y.fdl + (long long)q * R + (mq[q] & RM))
+                                       : X.at(Y.ga + ((long long)q * S + s) * R + (mq[q] & RM));
         const long long lo = imax(r, X.at(Y.gf + (long long)q * S + s));
         cand[q] = fit(X, Y.mb(w), nb_[w], cq[q], last, len, lo + dur) - dur;
       }
@@ -279,13 +322,13 @@ __device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
       if (bq < 0) break;
       const long long e = bt + dur;
       X.at(Y.gf + (long long)bq * S + s) = e;
-      X.at(Y.ga + ((long long)bq * S + s - 1) * M + mq[bq]) = e + wl2;
+      X.at(Y.ga + ((long long)bq * S + s - 1) * R + (mq[bq] & RM)) = e + wl2;
       last = e;
       ++mq[bq];
       cand[bq] = kInf64;
       if (mq[bq] < M) {
-        const long long r = s == S - 1 ? X.at(Y.fdl + (long long)bq * M + mq[bq])
-                                       : X.at(Y.ga + ((long long)bq * S + s) * M + mq[bq]);
+        const long long r = s == S - 1 ? X.at(Y.fdl + (long long)bq * R + (mq[bq] & RM))
+                                       : X.at(Y.ga + ((long long)bq * S + s) * R + (mq[bq] & RM));
         cand[bq] = fit(X, Y.mb(w), nb_[w], cq[bq], last, len, imax(r, e) + dur) - dur;
       }
       for (int q = 0; q < C; ++q)  // candidates pushed by the new reservation
@@ -298,10 +341,11 @@ __device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
   return mk;
 }
 
-__global__ void __launch_bounds__(kEvalThreads) atlas_seq_kernel(EvalArgs a) {
+template <int SMAX>
+__global__ void __launch_bounds__(kEvalThreads, 4) atlas_seq_kernel(EvalArgs a) {
   const int lane = threadIdx.x & 31;
   const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  SeqMem X{a.scratch + gwarp * a.scratch_per_warp + lane};  // [element][lane]
+  SeqMem X{a.scratch + gwarp * a.scratch_per_warp + (long long)lane * (a.scratch_per_warp / 32)};
   for (;;) {
     const int wk = atomicAdd(a.cursor, 1);
     if (wk >= a.n_work) break;
@@ -318,7 +362,7 @@ __global__ void __launch_bounds__(kEvalThreads) atlas_seq_kernel(EvalArgs a) {
     r.scenario = si;
     r.d = d;
     if (g.feasible) {
-      const long long mk = atlas_seq_row(g, sc.mem_limit, X);
+      const long long mk = atlas_seq_row<SMAX>(g, sc.mem_limit, X);
       finish_row(sc, tp, g, mk, r);
       if (mk < 0) {
         r.feasible = -1;
@@ -330,22 +374,34 @@ __global__ void __launch_bounds__(kEvalThreads) atlas_seq_kernel(EvalArgs a) {
   }
 }
 
-// int64 elements of one thread's slice for rows up to (C, S, M, nw)
-long long atlas_seq_slice(int C, int S, int M, int nw) {
-  return 2LL * C * S + (long long)C * M + (long long)C * S * M +
+// int64 elements of one thread's slice for rows up to (C, S, M, nw) with
+// memory cap L
+long long atlas_seq_slice(int C, int S, int M, int nw, int L) {
+  const long long R = seq_ring(L, M);
+  return 2LL * C * S + (long long)C * R + (long long)C * S * R +
          (long long)nw * (2LL * C * M + 2LL * M);
 }
 
-int atlas_seq_blocks_per_sm() {
+int atlas_seq_blocks_per_sm(int smax) {
   int n = 0;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_seq_kernel, kEvalThreads, 0) ==
-                 cudaSuccess
-             ? n
-             : 1;
+  const cudaError_t e =
+      smax <= 4 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_seq_kernel<4>,
+                                                                kEvalThreads, 0)
+      : smax <= 8 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_seq_kernel<8>,
+                                                                  kEvalThreads, 0)
+                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_seq_kernel<16>,
+                                                                  kEvalThreads, 0);
+  return e == cudaSuccess ? n : 1;
 }
 
-cudaError_t launch_atlas_seq(const EvalArgs& a, int grid, cudaStream_t st) {
-  atlas_seq_kernel<<<grid, kEvalThreads, 0, st>>>(a);
+// smax: 4, 8 or 16 (rows with S <= smax)
+cudaError_t launch_atlas_seq(int smax, const EvalArgs& a, int grid, cudaStream_t st) {
+  if (smax <= 4)
+    atlas_seq_kernel<4><<<grid, kEvalThreads, 0, st>>>(a);
+  else if (smax <= 8)
+    atlas_seq_kernel<8><<<grid, kEvalThreads, 0, st>>>(a);
+  else
+    atlas_seq_kernel<16><<<grid, kEvalThreads, 0, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -84,6 +84,11 @@ def load_library(path: str = LIB_PATH):
         "gpb_fetch_row_cycles": (C.c_int, [C.c_void_p, P(C.c_int64), C.c_int64]),
         "gpb_bucket_infos": (C.c_int, [C.c_void_p, P(abi.BucketInfo), C.c_int32,
                                        P(C.c_int32)]),
+        "gpb_saturating_requests": (C.c_int, [C.c_void_p, C.c_int64, P(abi.PrefillModel),
+                                              C.c_int64, P(abi.Request), C.c_int64,
+                                              P(C.c_int64)]),
+        "gpb_validate_timeline": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_int64), P(C.c_int64),
+                                            P(C.c_int32), P(C.c_int64)]),
         "gpb_group_create": (C.c_void_p, [C.c_int32, P(C.c_int32)]),
         "gpb_group_destroy": (None, [C.c_void_p]),
         "gpb_group_last_error": (C.c_char_p, [C.c_void_p]),
@@ -110,7 +115,8 @@ def exported_symbols():
             "gpb_synthetic_requests", "gpb_get_timing", "gpb_microbench", "gpb_set_stream",
             "gpb_copy_best", "gpb_set_profile", "gpb_fetch_row_cycles",
             "gpb_set_allreduce_tail", "gpb_timeline_arrays", "gpb_bucket_infos",
-            "gpb_set_bucket_timing", "gpb_group_create", "gpb_group_destroy",
+            "gpb_set_bucket_timing", "gpb_saturating_requests", "gpb_validate_timeline",
+            "gpb_group_create", "gpb_group_destroy",
             "gpb_group_last_error", "gpb_group_size", "gpb_group_load", "gpb_group_evaluate",
             "gpb_group_fetch_rows", "gpb_group_fetch_scenarios", "gpb_group_fetch_best"]
 
@@ -255,6 +261,36 @@ class Planner:
             if n.value <= cap:
                 return [(b.gpu_id, b.start_ns, b.end_ns) for b in out[: n.value]]
             cap = n.value
+
+    def timeline_arrays(self, row: int):
+        """(fe, ps, dims, makespan) of one row's timeline, cell 0
+        ([pipeline][stage][microbatch]; dims = (Ce, S, M, D))."""
+        dims = (C.c_int32 * 4)()
+        mk = C.c_int64()
+        self._check(self.lib.gpb_timeline_arrays(self.ctx, row, None, None, 0, dims,
+                                                 C.byref(mk)))
+        n = dims[0] * dims[1] * dims[2]
+        fe, ps = (C.c_int64 * n)(), (C.c_int64 * n)()
+        self._check(self.lib.gpb_timeline_arrays(self.ctx, row, fe, ps, n, dims, C.byref(mk)))
+        return fe, ps, tuple(dims), mk.value
+
+    def validate(self, row: int, fe=None, ps=None):
+        """validate_timeline (validate.h:77-256) on the device: (check, where)."""
+        chk, where = C.c_int32(), C.c_int64()
+        self._check(self.lib.gpb_validate_timeline(self.ctx, row, fe, ps, C.byref(chk),
+                                                   C.byref(where)))
+        return chk.value, where.value
+
+    def saturating_requests(self, row: int, pm=None, horizon_ns: int = 0):
+        """saturating_requests (bubbletea.cpp:240-267) computed on the device."""
+        pm = pm or abi.PrefillModel.default()
+        n = C.c_int64()
+        self._check(self.lib.gpb_saturating_requests(self.ctx, row, C.byref(pm), horizon_ns,
+                                                     None, 0, C.byref(n)))
+        out = (abi.Request * max(1, n.value))()
+        self._check(self.lib.gpb_saturating_requests(self.ctx, row, C.byref(pm), horizon_ns,
+                                                     out, n.value, C.byref(n)))
+        return out if n.value > 0 else (abi.Request * 0)()
 
     def pack_prefills(self, rows, reqs, pm=None, horizon_ns: int = 0, placements=False):
         pm = pm or abi.PrefillModel.default()

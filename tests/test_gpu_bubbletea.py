@@ -200,3 +200,31 @@ def test_pack_many_cells_zero_layer_stages(planner, checker):
         want, _ = checker.pack(tarr, scens[rows[top[0]].scenario], rows[top[0]].d, sat, pm,
                                placements=False)
         assert (got[0].accepted, got[0].placement_hash) == (want.accepted, want.placement_hash)
+
+
+@pytest.mark.parametrize("wide", [False, True])
+def test_saturating_requests_on_device(planner, checker, wide):
+    """saturating_requests (bubbletea.cpp:240-267) computed on the device from
+    the timeline's gap lists: the same requests (ids, arrival doubles, token
+    counts) as the reference, at the makespan and at other horizons."""
+    topos, scens = random_space(55 if wide else 56, 120, wide)
+    rng = random.Random(4)
+    pm = abi.PrefillModel.default()
+    n = 0
+    for i, r in _feasible_rows(planner, topos, scens, limit_gpus=2500):
+        if rng.random() > 0.3:
+            continue
+        sc = scens[r.scenario]
+        for hz in (0, max(1, r.makespan_ns // 3), r.makespan_ns + 7_000_001):
+            got = [(q.id, q.arrival_ms, q.tokens) for q in planner.saturating_requests(i, pm, hz)]
+            want = [(q.id, q.arrival_ms, q.tokens) for q in checker.saturating(topos, sc, r.d, pm, hz)]
+            assert got == want, (i, r.d, hz, abi.POLICY_NAMES[sc.policy], len(got), len(want))
+            n += 1
+    assert n > 20
+    # unit12 at M=5 (acceptance.cpp:221-252's stream)
+    topos, sc = fixtures.unit12(M=5, policy="atlas")
+    planner.load(topos, [sc])
+    planner.evaluate()
+    got = [(q.id, q.arrival_ms, q.tokens) for q in planner.saturating_requests(0, pm)]
+    assert got == [(q.id, q.arrival_ms, q.tokens) for q in checker.saturating(topos, sc, 1, pm)]
+    assert len(got) > 10

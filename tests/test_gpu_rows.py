@@ -191,3 +191,66 @@ def test_graph_mode_reloads(planner, checker, monkeypatch):
     assert _compare_space(planner, checker, None, topos, scens3[::-1]) > 120
     topos4, scens4 = random_space(99, 80, wide=True)
     assert _compare_space(planner, checker, None, topos4, scens4) > 80
+
+
+def test_validator_accepts_every_policy(planner):
+    """validate_timeline (validate.h:77-256) on the device: every feasible
+    row's own timeline is valid (completeness, GPU and link exclusivity,
+    causality, makespan)."""
+    import random
+    topos, scens = random_space(71, 150, wide=True)
+    planner.load(topos, scens)
+    planner.evaluate()
+    rows = planner.rows()
+    rng = random.Random(2)
+    seen = set()
+    n = 0
+    for i, r in enumerate(rows[:planner.n_rows]):
+        sc = scens[r.scenario]
+        if r.feasible != 1 or r.d * sc.pipelines_per_cell * sc.num_layers > 3000 or rng.random() > 0.4:
+            continue
+        assert planner.validate(i) == (0, 0), (i, abi.POLICY_NAMES[sc.policy])
+        seen.add(sc.policy)
+        n += 1
+    assert n > 40 and seen == {0, 1, 2, 3}
+
+
+def test_validator_rejects_corrupted_timelines(planner):
+    """The validator flags timelines corrupted to break completeness (check
+    1), GPU / link exclusivity or causality (checks 2-5: a moved task breaks
+    the first of them it meets) and the makespan (check 6), on unit12 (2
+    pipelines x 6 stages over 3 DCs) for ATLAS and gpipe."""
+    for pol in ("atlas", "gpipe"):
+        topos, sc = fixtures.unit12(policy=pol)
+        planner.load(topos, [sc])
+        planner.evaluate()
+        fe, ps, (Ce, S, M, D), mk = planner.timeline_arrays(0)
+        assert planner.validate(0) == (0, 0)
+        assert planner.validate(0, fe, ps) == (0, 0)
+        idx = lambda p, s, m: (p * S + s) * M + m  # noqa: E731
+
+        def corrupt(fn):
+            a, b = type(fe).from_buffer_copy(fe), type(ps).from_buffer_copy(ps)
+            fn(a, b)
+            return planner.validate(0, a, b)[0]
+
+        assert corrupt(lambda a, b: a.__setitem__(idx(0, 2, 1), -1)) == 1
+        assert corrupt(lambda a, b: b.__setitem__(idx(0, 3, 1), -1)) == 1
+        # a forward moved before its input, a pair before its gradient, a
+        # pair onto a forward
+        assert corrupt(lambda a, b: a.__setitem__(idx(0, 3, 0), a[idx(0, 2, 0)])) in (2, 3, 4)
+        assert corrupt(lambda a, b: b.__setitem__(idx(0, 2, M - 1), b[idx(0, 3, M - 1)])) in (2, 3, 5)
+        assert corrupt(lambda a, b: b.__setitem__(idx(0, 5, 0), a[idx(0, 5, 0)] - 1)) in (2, 5)
+        # the last pair (stage 0) pushed later: the makespan no longer matches
+        last = max(range(len(ps)), key=lambda k: ps[k])
+        assert (last // M) % S == 0
+        assert corrupt(lambda a, b: b.__setitem__(last, b[last] + 10**9)) == 6
+    # pooled link (ATLAS): pipeline 1's activation transfer on the first WAN
+    # boundary (stage 1 -> 2) moved onto pipeline 0's
+    topos, sc = fixtures.unit12(policy="atlas")
+    planner.load(topos, [sc])
+    planner.evaluate()
+    fe, ps, (Ce, S, M, D), mk = planner.timeline_arrays(0)
+    a, b = type(fe).from_buffer_copy(fe), type(ps).from_buffer_copy(ps)
+    a[(1 * S + 1) * M + 0] = a[(0 * S + 1) * M + 0]
+    assert planner.validate(0, a, b)[0] in (2, 3, 4)
