@@ -361,20 +361,71 @@ def space_measure(space, rank, world, reps=3, keep_rows=False):
         if buckets is None or ev[-1] == min(ev):
             buckets = p.bucket_infos()
     del flush
-    pinned = torch.empty(max(1, n) * ctypes.sizeof(abi.Row), dtype=torch.uint8, pin_memory=True)
-    out = (abi.Row * max(1, n)).from_address(pinned.data_ptr())
-    e2e = []
-    for _ in range(2):
-        t0 = time.perf_counter()
-        p.load(tarr, sarr)
-        p.evaluate(sync=False)
-        p._check(p.lib.gpb_fetch_rows(p.ctx, out, n))
-        e2e.append(time.perf_counter() - t0)
+    # e2e: K steps of load (host flatten + H2D) + evaluate + D2H of every row
+    # into pinned memory, two sessions alternating so step k+1's host work
+    # overlaps step k's evaluate (the evaluates stay serialised on the device)
+    p2 = Planner(torch_device_index())
+    e2e_s, out = e2e_pipelined([p, p2], tarr, sarr, n, steps=3)
     rows = (abi.Row * max(1, n)).from_buffer_copy(out) if keep_rows else None
+    p2.close()
     p.close()
+    e2e = [e2e_s]
     return {"rows": n, "scenarios": len(scens), "evaluate_ms": statistics.median(ev),
             "e2e_s": min(e2e), "ops": sum(b.algo_ops for b in buckets), "buckets": buckets,
             "topos": topos, "scens": scens, "row_list": rows}
+
+
+def e2e_pipelined(sessions, tarr, sarr, n_rows, steps, after_fetch=None):
+    """End-to-end steps through the C ABI: each step loads the space (host
+    flatten + H2D), evaluates it and reads every row back (D2H into pinned
+    memory). Sessions alternate on their own streams: step k+1's load runs
+    while step k evaluates; step k+1's evaluate waits for step k's end event,
+    so the device work per step equals the device-timed loop's. Returns
+    (seconds per step, the pinned rows of the last step)."""
+    import torch
+    from paper_2411_14458_b200 import abi
+    streams = [torch.cuda.Stream() for _ in sessions]
+    host = []
+    for p, st in zip(sessions, streams):
+        p.set_stream(st.cuda_stream)
+        p.set_bucket_timing(False)
+        pinned = torch.empty(max(1, n_rows) * ctypes.sizeof(abi.Row), dtype=torch.uint8,
+                             pin_memory=True)
+        host.append(((abi.Row * max(1, n_rows)).from_address(pinned.data_ptr()), pinned))
+
+    def launch(i, prev_end):
+        p, st = sessions[i % 2], streams[i % 2]
+        p.load(tarr, sarr)
+        if prev_end is not None:
+            st.wait_event(prev_end)
+        p.evaluate(sync=False)
+        end = torch.cuda.Event()
+        end.record(st)
+        return end
+
+    def finish(i):
+        p = sessions[i % 2]
+        rc = p.lib.gpb_fetch_rows(p.ctx, host[i % 2][0], n_rows)
+        assert rc == 0, p.lib.gpb_last_error(p.ctx)
+        if after_fetch is not None:
+            after_fetch(i, streams[i % 2])
+
+    def run(k):
+        prev = None
+        for i in range(k):
+            prev = launch(i, prev)
+            if i > 0:
+                finish(i - 1)
+        finish(k - 1)
+        torch.cuda.synchronize()
+
+    run(2)  # untimed: prepares each session's launch sequence
+    t0 = time.perf_counter()
+    run(steps)
+    dt = (time.perf_counter() - t0) / steps
+    for p in sessions:
+        p.set_stream(None)
+    return dt, host[(steps - 1) % 2][0]
 
 
 def bucket_rooflines(buckets, peak, top=4):
@@ -506,50 +557,17 @@ def impl_ours(args):
     # k+1's launch stream waits on step k's end event).
     e2e_steps = max(3, args.steps)
     planner2 = Planner(device)
-    sessions = [planner, planner2]
-    e2e_streams = [torch.cuda.Stream(), torch.cuda.Stream()]
-    host_rows = []
-    for p, s in zip(sessions, e2e_streams):
-        p.set_stream(s.cuda_stream)
-        p.set_bucket_timing(False)  # per-bucket profiling events: device-timed loop only
-        pinned = torch.empty(n_rows * ctypes.sizeof(abi.Row), dtype=torch.uint8,
-                             pin_memory=True)
-        host_rows.append(((abi.Row * n_rows).from_address(pinned.data_ptr()), pinned))
 
-    def e2e_launch(i, prev_end):
-        p, s = sessions[i % 2], e2e_streams[i % 2]
-        p.load(tarr, sarr)
-        if prev_end is not None:
-            s.wait_event(prev_end)
-        p.evaluate(sync=False)
-        end = torch.cuda.Event()
-        end.record(s)
-        return end
-
-    def e2e_finish(i):
-        p = sessions[i % 2]
-        rc = p.lib.gpb_fetch_rows(p.ctx, host_rows[i % 2][0], n_rows)
-        assert rc == 0, p.lib.gpb_last_error(p.ctx)
-        if world > 1:
-            with torch.cuda.stream(e2e_streams[i % 2]):
-                p.copy_best(best_t.data_ptr())
+    def exchange(i, st):
+        if world > 1:  # the 16-byte winners, ordered after the step's evaluate
+            with torch.cuda.stream(st):
+                [planner, planner2][i % 2].copy_best(best_t.data_ptr())
                 pdist.all_gather_best(best_t, world, gathered)
 
-    def e2e_run(k):
-        prev = None
-        for i in range(k):
-            prev = e2e_launch(i, prev)
-            if i > 0:
-                e2e_finish(i - 1)
-        e2e_finish(k - 1)
-        torch.cuda.synchronize()
-
-    e2e_run(4)  # untimed: prepares the second session's launch sequence
     if world > 1:
         dist.barrier()
-    t0 = time.perf_counter()
-    e2e_run(e2e_steps)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_s, _ = e2e_pipelined([planner, planner2], tarr, sarr, n_rows, e2e_steps,
+                             after_fetch=exchange)
     assert all(bytes(a) == bytes(b) for a, b in zip(rows0, planner2.rows())), \
         "second session rows differ"
     planner2.close()

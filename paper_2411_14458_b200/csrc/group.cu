@@ -213,10 +213,11 @@ int gpb_group_load(gpb_group* g, const gpb_topology* topos, int32_t n_topo,
   g->last_error.clear();
   g->loaded = g->evaluated = false;
   // validate the whole space once (same messages as a single-device load)
-  std::vector<DevTopo> dt;
-  std::vector<DevScen> ds;
+  std::vector<DevTopo> dt(std::max(n_topo, 1));
+  std::vector<DevScen> ds(std::max(n_scen, 1));
   int64_t n_rows = 0;
-  int rc = flatten_space(topos, n_topo, scens, n_scen, dt, ds, nullptr, n_rows, g->last_error);
+  int rc = flatten_space(topos, n_topo, scens, n_scen, dt.data(), ds.data(), nullptr, n_rows,
+                         g->last_error);
   if (rc != GPB_OK) return rc;
   const size_t n = g->ctx.size();
   // LPT over the devices by estimated cost, each shard in space order

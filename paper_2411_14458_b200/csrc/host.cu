@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -107,6 +108,7 @@ Ctx::~Ctx() {
     cudaEventDestroy(upload_ev);
   }
   if (stage) cudaFreeHost(stage);
+  if (stage_ts) cudaFreeHost(stage_ts);
   if (pack_side) cudaStreamDestroy(pack_side);
   if (pack_fork) cudaEventDestroy(pack_fork);
   if (pack_join) cudaEventDestroy(pack_join);
@@ -181,7 +183,7 @@ static void validate_scenario(const gpb_scenario& s, int idx, int n_topo,
     throw ConfigErr{"compute: durations must be positive"};  // workload.cpp:11-13
   }
   if (s.d_max < 0) throw ConfigErr{"select.d_max: must be >= 1"};
-  if (s.n_order < 0 || s.n_order > t.n_dc) throw ConfigErr{P() + ".n_order: out of range"};
+  if (s.n_order < 0 || s.n_order > GPB_MAX_DC) throw ConfigErr{P() + ".n_order: out of range"};
   unsigned seen = 0;
   for (int i = 0; i < s.n_order; ++i) {
     const int dc = s.dc_order[i];
@@ -288,14 +290,12 @@ static void parallel_chunks(int64_t n, int64_t min_chunk, Fn fn) {
 // large spaces; the error reported is the first one in input order
 // (topologies, then scenarios), as a sequential pass would find it.
 int flatten_space(const gpb_topology* topos, int32_t n_topo, const gpb_scenario* scens,
-                  int32_t n_scen, std::vector<DevTopo>& dt, std::vector<DevScen>& ds,
-                  std::vector<int32_t>* row_scen, int64_t& n_rows, std::string& err) {
+                  int32_t n_scen, DevTopo* dt, DevScen* ds, std::vector<int32_t>* row_scen,
+                  int64_t& n_rows, std::string& err) {
   if (n_scen < 0 || n_topo < 0 || (n_scen > 0 && (!topos || !scens))) {
     err = "null input";
     return GPB_CONFIG_ERROR;
   }
-  dt.assign(std::max(n_topo, 1), DevTopo());
-  ds.assign(std::max(n_scen, 1), DevScen());
   constexpr int kMaxThreads = 16;
   // first error per chunk: (input index, message); topologies before scenarios
   std::vector<std::pair<int64_t, std::string>> errs(kMaxThreads, {-1, ""});
@@ -423,6 +423,13 @@ static const bool kNoGroupFlush = std::getenv("GPB_NO_GROUP_FLUSH") != nullptr;
 // overrides, read at every load: tests force the grouped kernel)
 // one-thread ATLAS rows: per-thread slice bound (int64 elements, 256 KB)
 constexpr long long kSeqMaxSlice = 32768;
+// heavy ATLAS rows with 2..8 pipelines (S <= 32) run one CTA per row, one
+// warp per pipeline (atlas_wave_kernel); GPB_ATLAS_WAVE=0 disables, =2 sends
+// every such ATLAS row there (tests)
+static int atlas_wave_mode() {
+  const char* e = std::getenv("GPB_ATLAS_WAVE");
+  return e ? std::atoi(e) : 1;
+}
 static int atlas_seq_mode() {
   const char* e = std::getenv("GPB_ATLAS_SEQ");
   return e ? std::atoi(e) : 1;
@@ -457,14 +464,44 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
     c.set_error("null input");
     return GPB_CONFIG_ERROR;
   }
-  std::vector<DevTopo> dt;
-  std::vector<DevScen> ds;
+  // GPB_DEBUG_LOAD=1: host time of each load stage on stderr
+  static const bool dbg = std::getenv("GPB_DEBUG_LOAD") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto t_prev = now();
+  auto lap = [&](const char* what) {
+    if (!dbg) return;
+    const auto t = now();
+    std::fprintf(stderr, "gpb_load %-10s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t_prev).count());
+    t_prev = t;
+  };
+  // The topology and scenario tables are flattened straight into pinned
+  // staging (already resident: no page faults on 10^5-scenario spaces, no
+  // copy before the H2D); they stay the host view of the loaded space.
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t sz_t = sizeof(DevTopo) * std::max(n_topo, 1),
+               sz_s = sizeof(DevScen) * std::max(n_scen, 1);
+  if (c.upload_pending) {  // the previous upload must have left the staging buffers
+    cudaEventSynchronize(c.upload_ev);
+    c.upload_pending = false;
+  }
+  if (c.stage_ts_bytes < al(sz_t) + al(sz_s)) {
+    if (c.stage_ts) cudaFreeHost(c.stage_ts);
+    c.stage_ts = nullptr;
+    c.stage_ts_bytes = 0;
+    if (cudaMallocHost(&c.stage_ts, al(sz_t) + al(sz_s)) != cudaSuccess)
+      return c.cuda_fail(cudaErrorMemoryAllocation, "pinned staging");
+    c.stage_ts_bytes = al(sz_t) + al(sz_s);
+  }
+  DevTopo* dt = (DevTopo*)c.stage_ts;
+  DevScen* ds = (DevScen*)((unsigned char*)c.stage_ts + al(sz_t));
   int64_t n_rows = 0;
   {
     const int rc = flatten_space(topos, n_topo, scens, n_scen, dt, ds, nullptr, n_rows,
                                  c.last_error);
     if (rc != GPB_OK) return rc;
   }
+  lap("flatten");
 
   // Buckets: (policy, B = ceil(S/32)); within a bucket scenarios are dealt
   // in decreasing estimated cost so the persistent warps finish together.
@@ -501,10 +538,19 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
            (!heavy || seq_mode == 2) &&
            atlas_seq_slice(d.C, d.S, d.M, d.n_order - 1, d.mem_limit) <= kSeqMaxSlice;
   };
+  const int wave_mode = atlas_wave_mode();
+  auto wave_ok = [&](const DevScen& d, bool heavy) {
+    return wave_mode > 0 && (heavy || wave_mode == 2) && d.S <= 32 && d.C >= 2 &&
+           d.C <= kWaveMaxPipes;
+  };
   auto gw_of = [&](const DevScen& d, bool heavy) {
     // ATLAS: 32 = one warp per row, 4 / 8 / 16 = one thread per row with
-    // stage loops unrolled to that bound (atlas_seq_kernel<SMAX>)
-    if (d.policy == GPB_ATLAS) return seq_ok(d, heavy) ? (d.S <= 4 ? 4 : d.S <= 8 ? 8 : 16) : 32;
+    // stage loops unrolled to that bound (atlas_seq_kernel<SMAX>), 0 = one
+    // CTA per row with one warp per pipeline (atlas_wave_kernel)
+    if (d.policy == GPB_ATLAS) {
+      if (wave_ok(d, heavy)) return 0;
+      return seq_ok(d, heavy) ? (d.S <= 4 ? 4 : d.S <= 8 ? 8 : 16) : 32;
+    }
     if (kNoGroupFlush || n_rows < group_min) return 32;
     const int gw = d.S <= 8 ? 8 : (d.S <= 16 ? 16 : 32);
     // the per-row last-stage buffer (M entries per row) must fit the block
@@ -514,7 +560,8 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   for (int i = 0; i < n_scen; ++i) {
     int heavy = ds[i].policy == GPB_ATLAS && cost(i) >= 0.3 * max_atlas;
     const int gw = gw_of(ds[i], heavy != 0);
-    if (ds[i].policy == GPB_ATLAS && gw < 32) heavy = 0;
+    if (ds[i].policy == GPB_ATLAS && gw > 0 && gw < 32) heavy = 0;
+    if (ds[i].policy == GPB_ATLAS && gw == 0) heavy = 1;
     by_key[{ds[i].policy, (ds[i].S + 31) / 32, heavy, gw}].push_back(i);
   }
   std::vector<int32_t> bscen;
@@ -542,7 +589,7 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
       b.max_c = std::max(b.max_c, ds[i].C);
       b.max_s = std::max(b.max_s, ds[i].S);
       b.max_nw = std::max(b.max_nw, ds[i].n_order - 1);
-      if (b.policy == GPB_ATLAS && b.gw < 32)
+      if (b.policy == GPB_ATLAS && b.gw > 0 && b.gw < 32)
         b.max_slice = std::max(b.max_slice, atlas_seq_slice(ds[i].C, ds[i].S, ds[i].M,
                                                             ds[i].n_order - 1, ds[i].mem_limit));
     }
@@ -568,19 +615,14 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
     c.sel_blocks += b.sel_grid;
   }
 
+  lap("buckets");
   // Upload: the tables are written straight into one pinned staging buffer
   // (the per-row tables by several host threads) and copied asynchronously
   // on the launch stream (evaluate is ordered after them).
   cudaStream_t st = c.stream;
-  const size_t sz_t = sizeof(DevTopo) * dt.size(), sz_s = sizeof(DevScen) * ds.size(),
-               sz_r = sizeof(int32_t) * n_rows, sz_w = sizeof(int32_t) * n_work,
+  const size_t sz_r = sizeof(int32_t) * n_rows, sz_w = sizeof(int32_t) * n_work,
                sz_b = sizeof(int32_t) * bscen.size();
-  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  const size_t stage_need = al(sz_t) + al(sz_s) + al(sz_r) + al(sz_w) + al(sz_b);
-  if (c.upload_pending) {  // the previous upload must have left the staging buffer
-    cudaEventSynchronize(c.upload_ev);
-    c.upload_pending = false;
-  }
+  const size_t stage_need = al(sz_r) + al(sz_w) + al(sz_b);
   if (c.stage_bytes < stage_need) {
     if (c.stage) cudaFreeHost(c.stage);
     c.stage = nullptr;
@@ -591,14 +633,11 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   }
   if (!c.upload_ev && cudaEventCreateWithFlags(&c.upload_ev, cudaEventDisableTiming) != cudaSuccess)
     return c.cuda_fail(cudaGetLastError(), "event");
-  unsigned char* sp = (unsigned char*)c.stage;
-  unsigned char* st_t = sp;
-  unsigned char* st_s = st_t + al(sz_t);
-  int32_t* st_r = (int32_t*)(st_s + al(sz_s));
+  const unsigned char* st_t = (const unsigned char*)dt;
+  const unsigned char* st_s = (const unsigned char*)ds;
+  int32_t* st_r = (int32_t*)c.stage;
   int32_t* st_w = (int32_t*)((unsigned char*)st_r + al(sz_r));
   int32_t* st_b = (int32_t*)((unsigned char*)st_w + al(sz_w));
-  std::memcpy(st_t, dt.data(), sz_t);
-  std::memcpy(st_s, ds.data(), sz_s);
   std::memcpy(st_b, bscen.data(), sz_b);
   // row -> scenario and the bucket work lists (rows of each bucket scenario
   // in D order), one contiguous range of scenarios per host thread
@@ -611,6 +650,7 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
       for (int k = 0; k < d.n_rows; ++k) w[k] = (int32_t)(d.first_row + k);
     }
   });
+  lap("fill");
   auto up = [&](Buf& b, const void* src, size_t bytes) -> bool {
     void* p = c.dev_buf(b, bytes);
     if (!p) return false;
@@ -628,14 +668,16 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   }
   cudaEventRecord(c.upload_ev, st);
   c.upload_pending = true;
+  lap("upload");
   c.d2h_bytes = 0;
   c.h2d_bytes = sz_t + sz_s + sz_r + sz_w + sz_b;
   c.n_rows = n_rows;
   c.n_scen = n_scen;
   c.n_topo = n_topo;
-  c.dev_scens_host = std::move(ds);
-  c.dev_topos_host = std::move(dt);
+  c.dev_scens_host = ds;
+  c.dev_topos_host = dt;
   c.bscen_host = std::move(bscen);
+  lap("keep");
   // the launch sequence (ATLAS shapes, scratch, stream assignment) depends
   // only on the buckets' shapes: reuse it when a reload has the same ones.
   // A captured graph (GPB_GRAPH) also bakes in the scenario split of each
@@ -710,8 +752,9 @@ static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
       a.scratch_per_warp = P.scratch_per_warp;
       a.scratch_big_off = P.scratch_big_off;
       a.scratch = P.scratch_per_warp > 0 ? (long long*)c.b_scratch.ptr + c.scr_off[bi] : nullptr;
-      e = b.gw < 32 ? launch_atlas_seq(b.gw, a, P.grid, ss)
-                    : launch_atlas(b.B, a, P.grid, P.wpc, ss);
+      e = b.gw == 0   ? launch_atlas_wave(a, P.grid, P.wpc, ss)
+          : b.gw < 32 ? launch_atlas_seq(b.gw, a, P.grid, ss)
+                      : launch_atlas(b.B, a, P.grid, P.wpc, ss);
     }
     if (e != cudaSuccess) return c.cuda_fail(e, "eval launch");
     if (bt) rec(c.bucket_ev_end[bi], ss);
@@ -784,7 +827,21 @@ static int prepare_evaluate(Ctx& c) {
   for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
     const Bucket& b = c.buckets[bi];
     if (b.policy != GPB_ATLAS || b.count == 0) continue;
-    if (b.gw < 32) {  // one thread per row: a [element][lane] slice per thread
+    if (b.gw == 0) {  // one CTA per row, one warp per pipeline
+      AtlasPlan& P = c.aplan[bi];
+      const int rc = plan_atlas(c, 1, false, b.max_c, b.max_s, b.max_m, b.max_nw, b.max_csm, 1, P);
+      if (rc != GPB_OK) return rc;
+      if (atlas_wave_smem(P.L) > c.smem_optin) {
+        c.set_error("atlas wave plan too large for the shared-memory slice");
+        return GPB_CONFIG_ERROR;
+      }
+      P.wpc = b.max_c;
+      P.grid = std::max(1, std::min(b.count, c.num_sms));
+      c.scr_off[bi] = scr_total;
+      scr_total += (size_t)P.scratch_per_warp * P.grid;
+      continue;
+    }
+    if (b.gw < 32) {  // one thread per row: a per-thread slice
       AtlasPlan& P = c.aplan[bi];
       const long long slice = b.max_slice;
       P.wpc = kEvalThreads / 32;

@@ -69,8 +69,10 @@ struct Ctx {
   int32_t n_scen = 0, n_topo = 0;
   size_t h2d_bytes = 0;
   std::vector<Bucket> buckets;
-  std::vector<DevScen> dev_scens_host;
-  std::vector<DevTopo> dev_topos_host;
+  // host view of the loaded tables (in the pinned staging they were uploaded
+  // from; valid until the next gpb_load)
+  const DevScen* dev_scens_host = nullptr;
+  const DevTopo* dev_topos_host = nullptr;
   std::vector<int32_t> bscen_host;  // bucket scenario lists (Bucket::scen_off / scen_cnt)
   // scenario of a row: the last scenario whose first row is <= row
   int32_t scen_of_row(int64_t row) const {
@@ -125,8 +127,10 @@ struct Ctx {
   float pack_ms = 0.f;
   // pinned staging of the uploaded tables (async H2D; reused once the
   // previous upload has left it: upload_ev)
-  void* stage = nullptr;
+  void* stage = nullptr;  // row tables
   size_t stage_bytes = 0;
+  void* stage_ts = nullptr;  // topology + scenario tables
+  size_t stage_ts_bytes = 0;
   cudaEvent_t upload_ev = nullptr;
   bool upload_pending = false;
 
@@ -152,7 +156,7 @@ int row_wan_boundaries(const Ctx& c, int64_t row);
 // Validate + flatten a plan space on the host (multi-threaded for large
 // spaces); row_scen (nullable) receives the row -> scenario table.
 int flatten_space(const gpb_topology* topos, int32_t n_topo, const gpb_scenario* scens,
-                  int32_t n_scen, std::vector<DevTopo>& dt, std::vector<DevScen>& ds,
-                  std::vector<int32_t>* row_scen, int64_t& n_rows, std::string& err);
+                  int32_t n_scen, DevTopo* dt, DevScen* ds, std::vector<int32_t>* row_scen,
+                  int64_t& n_rows, std::string& err);
 
 }  // namespace gpb

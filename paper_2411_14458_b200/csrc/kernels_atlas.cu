@@ -244,6 +244,48 @@ __device__ __forceinline__ long long link_fit(const long long* mg, const int* jm
   }
 }
 
+// -inf of the max-plus maps (see the admission cascade below).
+constexpr long long kNegMP = -(1LL << 53);
+
+// Gradient-link queries of the admission cascade, per owned stage j (lane
+// stage j's WAN gradient link wbi[j]): conflict = free_at fails, fit =
+// earliest_fit (base.h:65-84), reserve = append to this pipeline's own list.
+// StaticLinks: the frozen pipelines' reservations merged into one list with
+// run jumps (one warp evaluates the pipelines in order).
+template <int B>
+struct StaticLinks {
+  const AtlasMem& X;
+  int C, M;
+  const int (&wbi)[B];
+  const long long (&ser)[B];
+  long long own[B];
+  LinkCur cur[B];
+  int n[B];
+  __device__ __forceinline__ StaticLinks(const AtlasMem& X_, int C_, int M_, const int (&wbi_)[B],
+                                         const long long (&ser_)[B])
+      : X(X_), C(C_), M(M_), wbi(wbi_), ser(ser_) {
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      own[j] = kNegMP;
+      n[j] = wbi[j] >= 0 ? X.mcnt[8 + wbi[j]] : 0;
+      cur[j].i = 0;
+      cur[j].v = kEndCur;
+      if (wbi[j] >= 0) cur[j].reset(X.mb + (size_t)wbi[j] * C * M, n[j]);
+    }
+  }
+  __device__ __forceinline__ bool conflict(int j, long long y) {
+    return link_conflict(X.mb + (size_t)wbi[j] * C * M, n[j], cur[j], own[j], ser[j], y);
+  }
+  __device__ __forceinline__ long long fit(int j, long long y) {
+    return link_fit(X.mb + (size_t)wbi[j] * C * M, X.jb + (size_t)wbi[j] * C * M, n[j], cur[j],
+                    own[j], ser[j], y);
+  }
+  __device__ __forceinline__ void reserve(int j, int p, int k, long long e) {
+    X.resb[((size_t)wbi[j] * C + p) * M + k] = e;
+    own[j] = e;
+  }
+};
+
 // ------------------------------------------------ admission cascade
 //
 // The memory-cap admission of microbatch m of pipeline p (scheduler.cpp:
@@ -273,23 +315,19 @@ __device__ __forceinline__ long long link_fit(const long long* mg, const int* jm
 // below 2^50 ns (13 days) and a composed map sums at most 256 terms (one
 // per stage), so plain adds never overflow (|sum| < 2^62) and a map that
 // includes a -inf term stays negative, below every real time (no clamping).
-constexpr long long kNegMP = -(1LL << 53);
 
 __device__ __forceinline__ long long mp_add(long long x, long long y) { return x + y; }
 
-template <int B, bool TIMELINE, bool PROF>
+template <int B, bool TIMELINE, bool PROF, typename Links>
 __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L, AtlasMem& X,
                                               long long (&gfr)[B], int (&drr)[B],
                                               const int (&wbi)[B], const long long (&serb)[B],
-                                              const long long (&latb)[B],
-                                              long long (&ownb)[B], LinkCur (&mcur)[B],
-                                              const int (&mn)[B], const long long (&wsuf)[B],
+                                              const long long (&latb)[B], Links& links,
+                                              const long long (&wsuf)[B],
                                               long long& n_pairs,
                                               long long& n_scans, long long& n_rounds,
                                               long long* cph) {
-  // ownb[j]: start of pipeline p's last reservation on stage j's gradient
-  // link (its own list tail); mcur/mn: cursor into / size of the link's
-  // static merged list — register copies, one lane owns each stage
+  // links: the gradient-link queries of the stages this lane owns
   long long ct = PROF ? clock64() : 0;
   const int lane = threadIdx.x & 31;
   const int S = g.S, M = g.M, C = g.C;
@@ -408,7 +446,7 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
         const int w = wbi[j];
         if (r < cnt[j] && w >= 0 && conf < 0) {
           const long long y = lo[j] + dur + dl[j];
-          if (link_conflict(X.mb + (size_t)w * C * M, mn[j], mcur[j], ownb[j], serb[j], y)) {
+          if (links.conflict(j, y)) {
             conf = j;
             conf_y = y;
           }
@@ -422,8 +460,7 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
 #pragma unroll
         for (int j = 0; j < B; ++j)
           if (j == conf) {
-            shift = link_fit(X.mb + (size_t)wbi[j] * C * M, X.jb + (size_t)wbi[j] * C * M, mn[j],
-                             mcur[j], ownb[j], serb[j], conf_y) - conf_y;
+            shift = links.fit(j, conf_y) - conf_y;
             dl[j] += shift;
           }
       }
@@ -449,10 +486,7 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
       const long long t = lo[j] + dl[j];
       const long long e = t + dur;
       gfr[j] = e;
-      if (wbi[j] >= 0) {  // reserve (append to list p)
-        X.resb[((size_t)wbi[j] * C + p) * M + k] = e;
-        ownb[j] = e;
-      }
+      if (wbi[j] >= 0) links.reserve(j, p, k, e);  // reserve (append to list p)
       if (s > 0) X.garr[((size_t)p * S + s - 1) * M + k] = e + wl[j];
       if (TIMELINE) X.ps[((size_t)p * S + s) * M + k] = t;
     }
@@ -843,17 +877,7 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
       }
     }
     __syncwarp();
-    long long ownb[B];
-    LinkCur mcur[B];
-    int mn[B];
-#pragma unroll
-    for (int j = 0; j < B; ++j) {
-      ownb[j] = kNegMP;
-      mn[j] = wbi[j] >= 0 ? X.mcnt[8 + wbi[j]] : 0;
-      mcur[j].i = 0;
-      mcur[j].v = kEndCur;
-      if (wbi[j] >= 0) mcur[j].reset(X.mb + (size_t)wbi[j] * C * M, mn[j]);
-    }
+    StaticLinks<B> links(X, C, M, wbi, serb);
     // lane w < nw: link w's constants for this pipeline (chain checks)
     long long aw_l = 0, lenw_l = 0, ownw_l = kNegMP;
     const long long* mgw_l = nullptr;
@@ -876,8 +900,8 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
         if (lane * B + j < S && m - drr[j] >= mem_limit) ++nblk;
       nblk = __reduce_add_sync(kFull, nblk);
       if (nblk > 0) {
-        atlas_cascade<B, TIMELINE, PROF>(g, p, m, mem_limit, X, gfr, drr, wbi, serb, latb, ownb,
-                                         mcur, mn, wsuf, n_pairs, n_stage_it, n_rounds, cph);
+        atlas_cascade<B, TIMELINE, PROF>(g, p, m, mem_limit, X, gfr, drr, wbi, serb, latb, links,
+                                         wsuf, n_pairs, n_stage_it, n_rounds, cph);
         if (PROF) ++n_adm;
       }
       if (PROF) {
@@ -1058,6 +1082,320 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
   long long mk = 0;
   for (int i = lane; i < C * S; i += 32) mk = imax(mk, X.gf[i]);
   return warp_max64(mk);
+}
+
+// ------------------------------------------------------ wave (heavy rows)
+//
+// The forward phase of the reference runs pipeline 0's M microbatches, then
+// pipeline 1's, ... (scheduler.cpp:362-431). Pipeline p reads the shared
+// links only through free_at / earliest_fit over the reservations of the
+// pipelines before it, and never affects them. So the pipelines can run
+// concurrently — one warp each, the whole CTA one row — provided pipeline p
+// waits, before it answers a query over the window [t, t + len) on a link,
+// until every earlier pipeline q has either finished its forward phase or
+// made a reservation on that link starting at or after t: q's reservations
+// on a link are appended in increasing time and all have length len, so
+// every later one then starts at or after t + len and cannot touch the
+// window. The answers are exactly those of the sequential order; the wait
+// chain only points to lower pipelines, so it cannot deadlock. The drain
+// (global greedy + per-stage decomposition) starts once every pipeline is
+// done, on warp 0, over the merged gradient lists. Used for the heavy ATLAS
+// rows (the critical path of a small space such as config 2: S=16, C=4,
+// M=64 went from one warp walking the 4 pipelines in turn to 4 warps).
+constexpr int kWaveMaxC = 8;
+
+struct WaveState {  // per CTA (one row), in shared memory
+  int cnt_f[GPB_MAX_DC - 1][kWaveMaxC];  // reservations per (link, pipeline)
+  int cnt_b[GPB_MAX_DC - 1][kWaveMaxC];
+  int done[kWaveMaxC];
+  int cur_f[kWaveMaxC][GPB_MAX_DC - 1][kWaveMaxC];  // pipeline p's cursors into list q
+  int cur_b[kWaveMaxC][GPB_MAX_DC - 1][kWaveMaxC];
+  int row;
+};
+
+__device__ __forceinline__ int vload(const int* p) { return *(const volatile int*)p; }
+__device__ __forceinline__ long long vload(const long long* p) {
+  return *(const volatile long long*)p;
+}
+
+// earliest t >= x with [t, t+len) free on the union of pipelines 0..p-1's
+// lists of one link (base + q*M, counts cnt[q], cursors cur[q]) and this
+// pipeline's own tail [own, own+len)
+__device__ long long wave_fit(const WaveState& W, const long long* base, int M, const int* cnt,
+                              int* cur, int p, long long own, long long len, long long x) {
+  if (len <= 0) return x;
+  long long t = x;
+  for (;;) {
+    bool moved = false;
+    for (int q = 0; q < p; ++q) {
+      const long long* L = base + (size_t)q * M;
+      int n;
+      for (;;) {  // wait for q's frontier to pass t (or q to finish)
+        n = vload(&cnt[q]);
+        if (n > 0 && vload(&L[n - 1]) >= t) break;
+        if (vload(&W.done[q])) {
+          n = vload(&cnt[q]);
+          break;
+        }
+        __nanosleep(32);
+      }
+      int c = cur[q];
+      while (c < n && vload(&L[c]) + len <= t) ++c;
+      cur[q] = c;
+      if (c < n && vload(&L[c]) < t + len) {
+        t = vload(&L[c]) + len;
+        moved = true;
+      }
+    }
+    if (own + len > t) {
+      t = own + len;
+      moved = true;
+    }
+    if (!moved) return t;
+  }
+}
+
+// gradient-link policy of the cascade (B = 1: the lane's one stage)
+struct WaveLinks {
+  AtlasMem& X;
+  WaveState& W;
+  int C, M, p, w;
+  long long len, own;
+  __device__ __forceinline__ long long fit(int, long long y) {
+    return wave_fit(W, X.resb + (size_t)w * C * M, M, W.cnt_b[w], W.cur_b[p][w], p, own, len, y);
+  }
+  __device__ __forceinline__ bool conflict(int j, long long y) { return len > 0 && fit(j, y) != y; }
+  __device__ __forceinline__ void reserve(int, int pp, int k, long long e) {
+    X.resb[((size_t)w * C + pp) * M + k] = e;
+    own = e;
+    __threadfence_block();
+    *(volatile int*)&W.cnt_b[w][pp] = k + 1;
+  }
+};
+
+// One pipeline's forward phase (the loop of atlas_row with wave queries).
+__device__ void atlas_wave_forward(const Geom& g, int mem_limit, AtlasMem& X, WaveState& W, int p,
+                                   const int (&wbi)[1], const int (&wfi)[1],
+                                   const long long (&serb)[1], const long long (&latb)[1],
+                                   const long long (&a_loc)[1], const long long (&wsuf)[1],
+                                   int wsrc) {
+  const int lane = threadIdx.x & 31;
+  const int S = g.S, M = g.M, C = g.C;
+  const long long f = g.fwd;
+  const int nw = g.nb - 1;
+  const int nl = S;  // B = 1
+  long long gfr[1] = {0};
+  int drr[1] = {0};
+  long long n0 = 0, n1 = 0, n2 = 0;
+  WaveLinks links{X, W, C, M, p, wbi[0] >= 0 ? wbi[0] : 0, serb[0], kNegMP};
+  if (wbi[0] < 0) links.len = 0;
+  for (int q = 0; q < kWaveMaxC; ++q)
+    for (int w = lane; w < nw; w += 32) W.cur_f[p][w][q] = W.cur_b[p][w][q] = 0;
+  long long aw_l = 0, lenw_l = 0, ownw_l = kNegMP;
+  if (lane < nw) {
+    aw_l = X.wa[lane];
+    lenw_l = X.wa[8 + lane];
+  }
+  __syncwarp();
+  for (int m = 0; m < M; ++m) {
+    const int nblk = __reduce_add_sync(kFull, lane < S && m - drr[0] >= mem_limit ? 1 : 0);
+    if (nblk > 0)
+      atlas_cascade<1, false, false>(g, p, m, mem_limit, X, gfr, drr, wbi, serb, latb, links,
+                                     wsuf, n0, n1, n2, nullptr);
+    long long gl = lane < S ? gfr[0] - a_loc[0] : -kInf64;
+    for (int o = 1; o < nl; o <<= 1) {
+      const long long v = shfl_up64(gl, o);
+      if (lane >= o) gl = imax(gl, v);
+    }
+    const long long gw = shfl_idx64(gl, wsrc);
+    long long t0 = __shfl_sync(kFull, gfr[0], 0);
+    if (nw > 0) {
+      for (;;) {
+        const long long e = aw_l + f + imax(t0, gw);
+        long long slot = e;
+        if (lane < nw)
+          slot = wave_fit(W, X.resf + (size_t)lane * C * M, M, W.cnt_f[lane], W.cur_f[p][lane],
+                          p, ownw_l, lenw_l, e);
+        const unsigned bal = __ballot_sync(kFull, lane < nw && slot != e);
+        if (!bal) break;
+        const int src = __ffs(bal) - 1;  // the lowest conflicting link shifts t0
+        t0 += shfl_idx64(slot - e, src);
+      }
+      if (lane < nw) {
+        ownw_l = aw_l + f + imax(t0, gw);
+        X.resf[((size_t)lane * C + p) * M + m] = ownw_l;
+        __threadfence_block();
+        *(volatile int*)&W.cnt_f[lane][p] = m + 1;
+      }
+    }
+    if (lane < S) {
+      const long long e = a_loc[0] + f + imax(t0, gl);
+      gfr[0] = e;
+      if (lane == S - 1) X.fdl[p * M + m] = e;
+    }
+    __syncwarp();
+  }
+  if (lane < S) {
+    X.gf[p * S + lane] = gfr[0];
+    X.nm[p * S + lane] = drr[0];
+  }
+  __threadfence_block();
+  __syncwarp();
+  if (lane == 0) *(volatile int*)&W.done[p] = 1;
+}
+
+// Drain phase of a row after the forward phases (warp 0): the gradient lists
+// of all pipelines merged per link, then the per-stage decomposition.
+template <int B, bool TIMELINE>
+__device__ long long atlas_drain_all(const Geom& g, AtlasMem& X, const WaveState* W) {
+  const int lane = threadIdx.x & 31;
+  const int S = g.S, M = g.M, C = g.C;
+  const int nw = g.nb - 1;
+  for (int i = lane; i < C * S; i += 32) X.firstm[i] = X.nm[i];
+  for (int w = 0; w < nw; ++w) {
+    int nbk = 0;
+    for (int q = 0; q < C; ++q) {
+      const int add_b = W ? W->cnt_b[w][q] : 0;
+      warp_merge(X.mb + (size_t)w * C * M, nbk, X.resb + ((size_t)w * C + q) * M, add_b, X.mtmp);
+      nbk += add_b;
+    }
+    warp_jumps(X.mb + (size_t)w * C * M, nbk, g.ser_pooled[w], X.jb + (size_t)w * C * M);
+    if (lane == 0) X.mcnt[8 + w] = nbk;
+    __syncwarp();
+  }
+  for (int s = S - 1; s >= 0;) {
+    const int w = X.wbs[s];
+    if (w >= 0) {
+      drain_stage_greedy<TIMELINE>(g, X, s, w);
+      --s;
+      continue;
+    }
+    int sb = s;
+    while (sb > 0 && X.wbs[sb - 1] < 0) --sb;
+    const int R = s - sb + 1, CM = C * g.M;
+    if ((long long)(CM + (R + B - 1) / B) > (long long)kWaveRatio * R * ((CM + 255) / 256)) {
+      for (; s >= sb; --s) drain_stage_scan<TIMELINE>(g, X, s);
+      continue;
+    }
+    constexpr int BW = B < 4 ? B : 4;
+    for (int st = s; st >= sb; st -= 32 * BW) {
+      const int bot = max(sb, st - 32 * BW + 1);
+      drain_run_wavefront<BW, TIMELINE>(g, X, st, bot);
+    }
+    s = sb - 1;
+  }
+  long long mk = 0;
+  for (int i = lane; i < C * S; i += 32) mk = imax(mk, X.gf[i]);
+  return warp_max64(mk);
+}
+
+// One CTA per heavy row (S <= 32, 2 <= C <= 8), warp p = pipeline p.
+__global__ void __launch_bounds__(32 * kWaveMaxC, 1) atlas_wave_kernel(EvalArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WaveState& W = *reinterpret_cast<WaveState*>(smem);
+  AtlasMem X;
+  long long* scr = a.scratch ? a.scratch + (size_t)blockIdx.x * a.scratch_per_warp : nullptr;
+  X.carve(smem + AtlasLayout::al(sizeof(WaveState)), a.lay, scr,
+          scr ? (unsigned char*)(scr + a.scratch_big_off) : nullptr);
+  for (;;) {
+    if (threadIdx.x == 0) W.row = atomicAdd(a.cursor, 1);
+    __syncthreads();
+    const int wk = W.row;
+    if (wk >= a.n_work) break;
+    const int row = a.work[wk];
+    const long long t_start = clock64();
+    Geom g;
+    const DevScen* sc;
+    const DevTopo* tp;
+    const bool ok = begin_row(a, row, g, sc, tp);  // warp 0's lane 0 writes infeasible rows
+    if (!ok) {
+      __syncthreads();
+      continue;
+    }
+    const int S = g.S, C = g.C;
+    const int nw = g.nb - 1;
+    X.garr = (long long)C * S * g.M <= X.garr_cap ? X.garr_smem : X.garr_glob;
+    if (warp == 0) {
+      for (int i = lane; i < C * S; i += 32) {
+        X.gf[i] = 0;
+        X.nm[i] = 0;
+      }
+      for (int s = lane; s < S; s += 32) {
+        int w;
+        X.wbs[s] = (s > 0 && wan_after(g, s - 1, w)) ? w : -1;
+      }
+      if (lane < nw) {
+        X.wa[8 + lane] = g.ser_pooled[lane];
+        X.wg[8 + lane] = g.lat[lane];
+      }
+      for (int i = lane; i < (GPB_MAX_DC - 1) * kWaveMaxC; i += 32) {
+        (&W.cnt_f[0][0])[i] = 0;
+        (&W.cnt_b[0][0])[i] = 0;
+      }
+      if (lane < kWaveMaxC) W.done[lane] = 0;
+    }
+    // every warp: its lane's stage (B = 1) constants
+    int wbi[1] = {-1}, wfi[1] = {-1};
+    long long serb[1] = {0}, latb[1] = {0}, a_loc[1] = {0}, wsuf[1] = {0};
+    {
+      const int s = lane;
+      long long run = 0, suf = 0;
+      if (s < S) {
+        int w;
+        if (s > 0 && wan_after(g, s - 1, w)) {
+          wbi[0] = w;
+          serb[0] = g.ser_pooled[w];
+          latb[0] = g.lat[w];
+        }
+        run = g.fwd;
+        if (s + 1 < S && wan_after(g, s, w)) {
+          run += g.ser_pooled[w] + g.lat[w];
+          wfi[0] = w;
+        }
+        suf = g.dur + (wbi[0] >= 0 ? serb[0] + latb[0] : 0);
+      }
+      long long incl = run;
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long v = shfl_up64(incl, o);
+        if (lane >= o) incl += v;
+      }
+      a_loc[0] = incl - run;
+      long long sincl = suf;
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long v = shfl_down64(sincl, o);
+        if (lane + o < 32) sincl += v;
+      }
+      wsuf[0] = sincl;
+    }
+    if (warp == 0 && wfi[0] >= 0) X.wa[wfi[0]] = a_loc[0];
+    const int wsrc = lane < nw ? g.blk_first[lane + 1] - 1 : lane;
+    __syncthreads();
+    if (warp < C)
+      atlas_wave_forward(g, sc->mem_limit, X, W, warp, wbi, wfi, serb, latb, a_loc, wsuf, wsrc);
+    __syncthreads();
+    if (warp == 0) {
+      const long long mk = atlas_drain_all<1, false>(g, X, &W);
+      int err = 0;
+      end_row(a, row, g, *sc, *tp, mk, err, t_start);
+    }
+    __syncthreads();
+  }
+}
+
+int atlas_wave_smem(const AtlasLayout& L) { return (int)(AtlasLayout::al(sizeof(WaveState)) + L.total); }
+
+cudaError_t launch_atlas_wave(const EvalArgs& a, int grid, int warps, cudaStream_t st) {
+  const int smem = atlas_wave_smem(a.lay);
+  static int set_to = 0;
+  if (smem > set_to) {
+    const cudaError_t e = cudaFuncSetAttribute(
+        atlas_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    set_to = smem;
+  }
+  atlas_wave_kernel<<<grid, 32 * warps, smem, st>>>(a);
+  return cudaGetLastError();
 }
 
 // Blocks per SM the register allocation must allow: 3 for one stage per lane

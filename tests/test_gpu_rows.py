@@ -254,3 +254,44 @@ def test_validator_rejects_corrupted_timelines(planner):
     a, b = type(fe).from_buffer_copy(fe), type(ps).from_buffer_copy(ps)
     a[(1 * S + 1) * M + 0] = a[(0 * S + 1) * M + 0]
     assert planner.validate(0, a, b)[0] in (2, 3, 4)
+
+
+def test_atlas_wave_rows_bit_exact(planner, checker, monkeypatch):
+    """Heavy ATLAS rows with 2..8 pipelines run one CTA per row, one warp per
+    pipeline, pipeline p waiting on the earlier pipelines' link frontiers
+    (atlas_wave_kernel); force it on every eligible row of the unit12 KATs,
+    random spaces with small memory caps, and config 2, and check each row
+    against the reference."""
+    import random
+    from oracle import bindings
+    from paper_2411_14458_b200 import workloads
+    monkeypatch.setenv("GPB_ATLAS_WAVE", "2")
+    for ml, ms in ((1, 89.0), (2, 67.0), (6, 36.0), (0, 36.0)):
+        topos, sc = fixtures.unit12(policy="atlas", mem_limit=ml)
+        assert planner.select(topos, sc).rows[0].pp_time_ms == ms
+    rng = random.Random(9)
+    topos, scens = [], []
+    for _ in range(80):
+        n_dc = rng.randint(2, 5)
+        counts = [rng.choice([64, 128, 256]) for _ in range(n_dc)]
+        lat = [[0.0] * n_dc for _ in range(n_dc)]
+        for i in range(n_dc):
+            for j in range(i + 1, n_dc):
+                lat[i][j] = lat[j][i] = rng.choice([5.0, 20.0, 80.0])
+        topos.append(abi.make_topology(counts, cap_gbps=rng.choice([1.0, 5.0, 25.0]),
+                                       intra_gbps=100.0, latency=lat))
+        S = rng.randint(2, 32)
+        scens.append(abi.make_scenario(
+            topology=len(topos) - 1, policy="atlas", num_layers=S,
+            num_microbatches=rng.choice([2, 7, 16, 64]),
+            hidden=rng.choice([1024, 4096]), seq_len=rng.choice([1024, 4096]),
+            fwd_ms=rng.uniform(1.0, 20.0), bwd_ms=rng.uniform(2.0, 40.0),
+            recompute_ms=rng.uniform(0.0, 10.0), C=rng.choice([2, 3, 4, 8]),
+            recompute=rng.random() < 0.5, multi_conn=rng.random() < 0.5,
+            mem_limit=rng.choice([0, 1, 2, 5, S]), d_max=1, dc_order=list(range(n_dc))))
+    assert _compare_space(planner, checker, bindings.port(), abi.array(abi.Topology, topos),
+                          abi.array(abi.Scenario, scens)) == 80
+    topos, scens = workloads.config2(3000, seed=7)
+    scens = [s for s in scens if s.policy == 3]
+    assert _compare_space(planner, checker, bindings.port(), abi.array(abi.Topology, topos),
+                          abi.array(abi.Scenario, scens)) > 500

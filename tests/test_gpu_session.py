@@ -143,3 +143,62 @@ def test_sharded_selection_byte_identical(libs, tmp_path, monkeypatch, cfg, cmd)
     assert ra[:2] == rb[:2], (ra, rb)
     fa, fb = _files(a), _files(b)
     assert fa.keys() == fb.keys() and all(fa[k] == fb[k] for k in fa)
+
+
+def _doc(n_dc=2, gpus=64, layers=4, lpp=1, M=4, C=1, policy="atlas", dc_order=None,
+         bwd_ms=20.0, rec_ms=10.0):
+    import json
+    dcs = [{"id": f"dc{i}", "gpu_count": gpus, "intra_bw_gbps": 100.0} for i in range(n_dc)]
+    lat = {f"dc{i}|dc{j}": 10.0 + i + j for i in range(n_dc) for j in range(i + 1, n_dc)}
+    sel = {"policy": policy, "pipelines_per_cell": C, "d_max": 1}
+    if dc_order is not None:
+        sel["dc_order"] = dc_order
+    doc = {"datacenters": dcs, "wan": {"latency_ms": lat, "pair_bw_cap_gbps": 5.0},
+           "model": {"num_layers": layers, "layers_per_partition": lpp, "hidden": 512,
+                     "seq_len": 512, "num_microbatches": M},
+           "compute": {"fwd_ms": 10.0, "bwd_ms": bwd_ms, "recompute_ms": rec_ms},
+           "parallelism": {"pipelines_per_cell": C}, "select": sel}
+    return json.dumps(doc).encode()
+
+
+def _run_text(path, text, out):
+    s = Session(path)
+    try:
+        assert s.load_config_text(text) == 0
+        rc = s.run_select_dc(out.encode())
+        return rc, s.last_error().decode()
+    finally:
+        s.close()
+
+
+def test_envelope_rc_parity(libs, tmp_path):
+    """The kernel envelope through gp_run_select_dc, beside the
+    reference's own rc. At each boundary the reference's input is accepted
+    with identical bytes; one step beyond it ours returns GP_CONFIG_ERROR
+    naming the envelope (a loud, documented divergence: the reference
+    accepts these inputs), never a silent difference."""
+    ref_so, ours = libs
+    inside = [
+        ("8 datacenters", _doc(n_dc=8, gpus=8, layers=8)),
+        ("256 stages", _doc(n_dc=2, gpus=256, layers=256, M=2)),
+        ("32 atlas pipelines", _doc(n_dc=2, gpus=64, layers=2, C=32, M=2)),
+        ("1 ns pairs", _doc(bwd_ms=1e-6, rec_ms=0.0)),
+    ]
+    for name, text in inside:
+        a, b = tmp_path / f"ref_{len(name)}", tmp_path / f"ours_{len(name)}"
+        ra, rb = _run_text(ref_so, text, str(a)), _run_text(ours, text, str(b))
+        assert ra[0] == rb[0] == 0, (name, ra, rb)
+        assert _files(a) == _files(b), name
+    beyond = [
+        ("9 datacenters", _doc(n_dc=9, gpus=8, layers=9), "more than 8 datacenters"),
+        ("257 stages", _doc(n_dc=2, gpus=256, layers=257, M=2), "256 pipeline stages"),
+        ("33 atlas pipelines", _doc(n_dc=2, gpus=66, layers=2, C=33, M=2), "32 pipelines"),
+        ("0 ns pairs", _doc(bwd_ms=1e-7, rec_ms=0.0), "0 ns"),
+        ("duplicate dc_order", _doc(n_dc=2, gpus=64, layers=4, dc_order=["dc0", "dc1", "dc0"]),
+         "duplicate"),
+    ]
+    for name, text, why in beyond:
+        ra = _run_text(ref_so, text, str(tmp_path / "r"))
+        rb = _run_text(ours, text, str(tmp_path / "o"))
+        assert ra[0] == 0, (name, ra)  # the reference accepts it
+        assert rb[0] == 2 and why in rb[1], (name, rb)
