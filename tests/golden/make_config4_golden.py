@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 from oracle import bindings  # noqa: E402
 from paper_2411_14458_b200 import abi, workloads  # noqa: E402
 
-OUT = os.path.join(ROOT, "tests", "golden", "config4_pack.json")
+OUT = os.environ.get("GOLDEN_OUT", os.path.join(ROOT, "tests", "golden", "config4_pack.json"))
 N_TRACE, SEED = 1_000_000, 42
 
 
