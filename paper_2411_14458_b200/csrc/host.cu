@@ -836,7 +836,8 @@ static int prepare_evaluate(Ctx& c) {
         return GPB_CONFIG_ERROR;
       }
       P.wpc = b.max_c;
-      P.grid = std::max(1, std::min(b.count, c.num_sms));
+      const int per_sm = std::max(1, atlas_wave_blocks_per_sm(P.wpc, atlas_wave_smem(P.L)));
+      P.grid = std::max(1, std::min(b.count, c.num_sms * per_sm));
       c.scr_off[bi] = scr_total;
       scr_total += (size_t)P.scratch_per_warp * P.grid;
       continue;

@@ -65,6 +65,7 @@ long long atlas_seq_slice(int C, int S, int M, int nw, int L);
 // the AtlasLayout slice (+ wave state) per CTA, scratch_per_warp per CTA
 constexpr int kWaveMaxPipes = 8;
 int atlas_wave_smem(const AtlasLayout& L);
+int atlas_wave_blocks_per_sm(int warps, int smem);
 cudaError_t launch_atlas_wave(const EvalArgs& a, int grid, int warps, cudaStream_t st);
 int atlas_seq_blocks_per_sm(int smax);
 cudaError_t launch_atlas_seq(int smax, const EvalArgs& a, int grid, cudaStream_t st);

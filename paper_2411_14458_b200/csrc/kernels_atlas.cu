@@ -1111,6 +1111,7 @@ struct WaveState {  // per CTA (one row), in shared memory
   int cur_f[kWaveMaxC][GPB_MAX_DC - 1][kWaveMaxC];  // pipeline p's cursors into list q
   int cur_b[kWaveMaxC][GPB_MAX_DC - 1][kWaveMaxC];
   int row;
+  unsigned long long wait_cyc[kWaveMaxC];  // profiling: cycles pipeline p spent waiting
 };
 
 __device__ __forceinline__ int vload(const int* p) { return *(const volatile int*)p; }
@@ -1118,10 +1119,30 @@ __device__ __forceinline__ long long vload(const long long* p) {
   return *(const volatile long long*)p;
 }
 
+// Wait until list q (of a link, counts cnt[q]) is final below t: q finished,
+// or its last reservation starts at or after t. Returns its length.
+__device__ __forceinline__ int wave_wait(WaveState& W, const long long* L, const int* cnt, int q,
+                                         int p, long long t) {
+  int n = vload(&cnt[q]);
+  if (n > 0 && vload(&L[n - 1]) >= t) return n;
+  const long long t0 = clock64();
+  for (;;) {
+    n = vload(&cnt[q]);
+    if (n > 0 && vload(&L[n - 1]) >= t) break;
+    if (vload(&W.done[q])) {
+      n = vload(&cnt[q]);
+      break;
+    }
+    __nanosleep(20);
+  }
+  atomicAdd(&W.wait_cyc[p], (unsigned long long)(clock64() - t0));
+  return n;
+}
+
 // earliest t >= x with [t, t+len) free on the union of pipelines 0..p-1's
 // lists of one link (base + q*M, counts cnt[q], cursors cur[q]) and this
 // pipeline's own tail [own, own+len)
-__device__ long long wave_fit(const WaveState& W, const long long* base, int M, const int* cnt,
+__device__ long long wave_fit(WaveState& W, const long long* base, int M, const int* cnt,
                               int* cur, int p, long long own, long long len, long long x) {
   if (len <= 0) return x;
   long long t = x;
@@ -1129,16 +1150,7 @@ __device__ long long wave_fit(const WaveState& W, const long long* base, int M, 
     bool moved = false;
     for (int q = 0; q < p; ++q) {
       const long long* L = base + (size_t)q * M;
-      int n;
-      for (;;) {  // wait for q's frontier to pass t (or q to finish)
-        n = vload(&cnt[q]);
-        if (n > 0 && vload(&L[n - 1]) >= t) break;
-        if (vload(&W.done[q])) {
-          n = vload(&cnt[q]);
-          break;
-        }
-        __nanosleep(32);
-      }
+      const int n = wave_wait(W, L, cnt, q, p, t);
       int c = cur[q];
       while (c < n && vload(&L[c]) + len <= t) ++c;
       cur[q] = c;
@@ -1155,6 +1167,23 @@ __device__ long long wave_fit(const WaveState& W, const long long* base, int M, 
   }
 }
 
+// free_at(x, x+len) on the same union: waits as wave_fit, but moves the
+// cursors only past reservations ending at or before x (a later wave_fit from
+// x must still see everything overlapping [x, ...))
+__device__ bool wave_conflict(WaveState& W, const long long* base, int M, const int* cnt,
+                              int* cur, int p, long long own, long long len, long long x) {
+  if (len <= 0) return false;
+  for (int q = 0; q < p; ++q) {
+    const long long* L = base + (size_t)q * M;
+    const int n = wave_wait(W, L, cnt, q, p, x);
+    int c = cur[q];
+    while (c < n && vload(&L[c]) + len <= x) ++c;
+    cur[q] = c;
+    if (c < n && vload(&L[c]) < x + len) return true;
+  }
+  return own + len > x;
+}
+
 // gradient-link policy of the cascade (B = 1: the lane's one stage)
 struct WaveLinks {
   AtlasMem& X;
@@ -1164,7 +1193,10 @@ struct WaveLinks {
   __device__ __forceinline__ long long fit(int, long long y) {
     return wave_fit(W, X.resb + (size_t)w * C * M, M, W.cnt_b[w], W.cur_b[p][w], p, own, len, y);
   }
-  __device__ __forceinline__ bool conflict(int j, long long y) { return len > 0 && fit(j, y) != y; }
+  __device__ __forceinline__ bool conflict(int, long long y) {
+    return wave_conflict(W, X.resb + (size_t)w * C * M, M, W.cnt_b[w], W.cur_b[p][w], p, own, len,
+                         y);
+  }
   __device__ __forceinline__ void reserve(int, int pp, int k, long long e) {
     X.resb[((size_t)w * C + pp) * M + k] = e;
     own = e;
@@ -1212,14 +1244,17 @@ __device__ void atlas_wave_forward(const Geom& g, int mem_limit, AtlasMem& X, Wa
     if (nw > 0) {
       for (;;) {
         const long long e = aw_l + f + imax(t0, gw);
-        long long slot = e;
-        if (lane < nw)
-          slot = wave_fit(W, X.resf + (size_t)lane * C * M, M, W.cnt_f[lane], W.cur_f[p][lane],
-                          p, ownw_l, lenw_l, e);
-        const unsigned bal = __ballot_sync(kFull, lane < nw && slot != e);
+        const bool conf = lane < nw && wave_conflict(W, X.resf + (size_t)lane * C * M, M,
+                                                     W.cnt_f[lane], W.cur_f[p][lane], p, ownw_l,
+                                                     lenw_l, e);
+        const unsigned bal = __ballot_sync(kFull, conf);
         if (!bal) break;
         const int src = __ffs(bal) - 1;  // the lowest conflicting link shifts t0
-        t0 += shfl_idx64(slot - e, src);
+        long long shift = 0;
+        if (lane == src)
+          shift = wave_fit(W, X.resf + (size_t)lane * C * M, M, W.cnt_f[lane], W.cur_f[p][lane],
+                           p, ownw_l, lenw_l, e) - e;
+        t0 += shfl_idx64(shift, src);
       }
       if (lane < nw) {
         ownw_l = aw_l + f + imax(t0, gw);
@@ -1333,7 +1368,10 @@ __global__ void __launch_bounds__(32 * kWaveMaxC, 1) atlas_wave_kernel(EvalArgs 
         (&W.cnt_f[0][0])[i] = 0;
         (&W.cnt_b[0][0])[i] = 0;
       }
-      if (lane < kWaveMaxC) W.done[lane] = 0;
+      if (lane < kWaveMaxC) {
+        W.done[lane] = 0;
+        W.wait_cyc[lane] = 0;
+      }
     }
     // every warp: its lane's stage (B = 1) constants
     int wbi[1] = {-1}, wfi[1] = {-1};
@@ -1371,19 +1409,39 @@ __global__ void __launch_bounds__(32 * kWaveMaxC, 1) atlas_wave_kernel(EvalArgs 
     if (warp == 0 && wfi[0] >= 0) X.wa[wfi[0]] = a_loc[0];
     const int wsrc = lane < nw ? g.blk_first[lane + 1] - 1 : lane;
     __syncthreads();
+    const long long t_fwd = clock64();
     if (warp < C)
       atlas_wave_forward(g, sc->mem_limit, X, W, warp, wbi, wfi, serb, latb, a_loc, wsuf, wsrc);
+    const long long t_fwd_end = clock64();
     __syncthreads();
     if (warp == 0) {
+      const long long t_drain = clock64();
       const long long mk = atlas_drain_all<1, false>(g, X, &W);
       int err = 0;
       end_row(a, row, g, *sc, *tp, mk, err, t_start);
+      if (a.row_phase && lane == 0) {  // profiling: forward / drain / per-pipeline waits
+        long long* ph = a.row_phase + 16 * (size_t)row;
+        ph[0] = t_drain - t_fwd;
+        ph[3] = clock64() - t_drain;
+        for (int q = 0; q < kWaveMaxC; ++q) ph[8 + q] = (long long)W.wait_cyc[q];
+      }
     }
+    if (a.row_phase && lane == 0 && warp < C && warp < 4)
+      a.row_phase[16 * (size_t)row + 4 + warp] = t_fwd_end - t_fwd;
     __syncthreads();
   }
 }
 
 int atlas_wave_smem(const AtlasLayout& L) { return (int)(AtlasLayout::al(sizeof(WaveState)) + L.total); }
+
+int atlas_wave_blocks_per_sm(int warps, int smem) {
+  cudaFuncSetAttribute(atlas_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int n = 0;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_wave_kernel, 32 * warps, smem) ==
+                 cudaSuccess
+             ? n
+             : 1;
+}
 
 cudaError_t launch_atlas_wave(const EvalArgs& a, int grid, int warps, cudaStream_t st) {
   const int smem = atlas_wave_smem(a.lay);
