@@ -423,12 +423,16 @@ static const bool kNoGroupFlush = std::getenv("GPB_NO_GROUP_FLUSH") != nullptr;
 // overrides, read at every load: tests force the grouped kernel)
 // one-thread ATLAS rows: per-thread slice bound (int64 elements, 256 KB)
 constexpr long long kSeqMaxSlice = 32768;
-// heavy ATLAS rows with 2..8 pipelines (S <= 32) run one CTA per row, one
-// warp per pipeline (atlas_wave_kernel); GPB_ATLAS_WAVE=0 disables, =2 sends
-// every such ATLAS row there (tests)
+// heavy ATLAS rows with 2..8 pipelines (S <= 32) can run one CTA per row, one
+// warp per pipeline (atlas_wave_kernel): GPB_ATLAS_WAVE=1 for heavy rows, =2
+// for every such ATLAS row (tests). Off by default: measured on config 2 the
+// union-of-lists queries cost more than the pipeline concurrency saves (the
+// critical S=16, C=4, M=64 row: 1.03 M cycles on one warp, 1.87 M on the wave;
+// pipeline 3 spends 0.71 M cycles waiting on the frontiers of 0..2 and 1.06 M
+// in its own queries; profiles/r02_summary.md).
 static int atlas_wave_mode() {
   const char* e = std::getenv("GPB_ATLAS_WAVE");
-  return e ? std::atoi(e) : 1;
+  return e ? std::atoi(e) : 0;
 }
 static int atlas_seq_mode() {
   const char* e = std::getenv("GPB_ATLAS_SEQ");
