@@ -423,13 +423,15 @@ static const bool kNoGroupFlush = std::getenv("GPB_NO_GROUP_FLUSH") != nullptr;
 // overrides, read at every load: tests force the grouped kernel)
 // one-thread ATLAS rows: per-thread slice bound (int64 elements, 256 KB)
 constexpr long long kSeqMaxSlice = 32768;
-// heavy ATLAS rows with 2..8 pipelines (S <= 32) can run one CTA per row, one
+// heavy ATLAS rows with 2..4 pipelines (S <= 32) can run one CTA per row, one
 // warp per pipeline (atlas_wave_kernel): GPB_ATLAS_WAVE=1 for heavy rows, =2
-// for every such ATLAS row (tests). Off by default: measured on config 2 the
-// union-of-lists queries cost more than the pipeline concurrency saves (the
-// critical S=16, C=4, M=64 row: 1.03 M cycles on one warp, 1.87 M on the wave;
-// pipeline 3 spends 0.71 M cycles waiting on the frontiers of 0..2 and 1.06 M
-// in its own queries; profiles/r02_summary.md).
+// for every such ATLAS row (tests). Off by default: on config 2's critical
+// row (S=16, C=4, M=64) pipeline p's microbatches sit far later in simulated
+// time than p-1's (the pooled links are saturated by the earlier pipelines),
+// so p trails p-1 by ~40-60 microbatches of work and the staircase of
+// frontier waits leaves little concurrency: 0.96 M cycles on the wave vs
+// 1.03 M on one warp (profiles/r02_summary.md), within run-to-run noise of
+// the step.
 static int atlas_wave_mode() {
   const char* e = std::getenv("GPB_ATLAS_WAVE");
   return e ? std::atoi(e) : 0;
@@ -850,7 +852,8 @@ static int prepare_evaluate(Ctx& c) {
       AtlasPlan& P = c.aplan[bi];
       const long long slice = b.max_slice;
       P.wpc = kEvalThreads / 32;
-      const long long per_sm = std::max(1, atlas_seq_blocks_per_sm(b.gw));
+      long long per_sm = std::max(1, atlas_seq_blocks_per_sm(b.gw));
+      if (const char* e = std::getenv("GPB_SEQ_PER_SM")) per_sm = std::max(1, std::atoi(e));
       long long grid = std::min<long long>((long long)c.num_sms * per_sm,
                                            (b.count + kEvalThreads - 1) / kEvalThreads);
       // scratch bound: 12 GiB per bucket (rows beyond the resident ones reuse it)

@@ -61,9 +61,9 @@ int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem);
 // one thread per ATLAS row (bulk of large spaces); scratch_per_warp = 32 x
 // the per-thread slice (int64 elements) for rows up to (C, S, M, nw)
 long long atlas_seq_slice(int C, int S, int M, int nw, int L);
-// heavy ATLAS rows (S <= 32, 2 <= C <= 8): one CTA per row, warp = pipeline;
+// heavy ATLAS rows (S <= 32, 2 <= C <= 4): one CTA per row, warp = pipeline;
 // the AtlasLayout slice (+ wave state) per CTA, scratch_per_warp per CTA
-constexpr int kWaveMaxPipes = 8;
+constexpr int kWaveMaxPipes = 4;  // = kWaveRegC (register-cached list views)
 int atlas_wave_smem(const AtlasLayout& L);
 int atlas_wave_blocks_per_sm(int warps, int smem);
 cudaError_t launch_atlas_wave(const EvalArgs& a, int grid, int warps, cudaStream_t st);

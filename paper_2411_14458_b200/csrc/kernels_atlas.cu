@@ -1108,8 +1108,6 @@ struct WaveState {  // per CTA (one row), in shared memory
   int cnt_f[GPB_MAX_DC - 1][kWaveMaxC];  // reservations per (link, pipeline)
   int cnt_b[GPB_MAX_DC - 1][kWaveMaxC];
   int done[kWaveMaxC];
-  int cur_f[kWaveMaxC][GPB_MAX_DC - 1][kWaveMaxC];  // pipeline p's cursors into list q
-  int cur_b[kWaveMaxC][GPB_MAX_DC - 1][kWaveMaxC];
   int row;
   unsigned long long wait_cyc[kWaveMaxC];  // profiling: cycles pipeline p spent waiting
 };
@@ -1119,83 +1117,114 @@ __device__ __forceinline__ long long vload(const long long* p) {
   return *(const volatile long long*)p;
 }
 
-// Wait until list q (of a link, counts cnt[q]) is final below t: q finished,
-// or its last reservation starts at or after t. Returns its length.
-__device__ __forceinline__ int wave_wait(WaveState& W, const long long* L, const int* cnt, int q,
-                                         int p, long long t) {
-  int n = vload(&cnt[q]);
-  if (n > 0 && vload(&L[n - 1]) >= t) return n;
-  const long long t0 = clock64();
-  for (;;) {
-    n = vload(&cnt[q]);
-    if (n > 0 && vload(&L[n - 1]) >= t) break;
-    if (vload(&W.done[q])) {
-      n = vload(&cnt[q]);
-      break;
+// One lane's view of one link's lists of the pipelines before it, with the
+// cursor position and entry, the list length and the time below which the
+// list is known final held in registers (the common query reads no memory,
+// as atlas_kernel's static cursor does). NQ >= the number of earlier
+// pipelines (the wave kernel takes C <= kWaveRegC).
+constexpr int kWaveRegC = 4;
+template <int NQ>
+struct WaveView {
+  const long long* base;  // list q at base + q * M
+  const int* cnt;         // published lengths
+  const int* done;        // per pipeline: forward phase finished
+  int M, p;
+  int n[NQ], idx[NQ];
+  long long val[NQ], fin[NQ];
+  __device__ __forceinline__ void init(const long long* b, const int* c, const int* d, int M_,
+                                       int p_) {
+    base = b;
+    cnt = c;
+    done = d;
+    M = M_;
+    p = p_;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      n[q] = idx[q] = 0;
+      val[q] = kEndCur;
+      fin[q] = kNegMP;
     }
-    __nanosleep(20);
   }
-  atomicAdd(&W.wait_cyc[p], (unsigned long long)(clock64() - t0));
-  return n;
-}
-
-// earliest t >= x with [t, t+len) free on the union of pipelines 0..p-1's
-// lists of one link (base + q*M, counts cnt[q], cursors cur[q]) and this
-// pipeline's own tail [own, own+len)
-__device__ long long wave_fit(WaveState& W, const long long* base, int M, const int* cnt,
-                              int* cur, int p, long long own, long long len, long long x) {
-  if (len <= 0) return x;
-  long long t = x;
-  for (;;) {
-    bool moved = false;
-    for (int q = 0; q < p; ++q) {
-      const long long* L = base + (size_t)q * M;
-      const int n = wave_wait(W, L, cnt, q, p, t);
-      int c = cur[q];
-      while (c < n && vload(&L[c]) + len <= t) ++c;
-      cur[q] = c;
-      if (c < n && vload(&L[c]) < t + len) {
-        t = vload(&L[c]) + len;
+  // list q final below t (q done, or its last reservation starts at or
+  // after t: every later one starts at or after t + len)
+  __device__ __forceinline__ void ensure(int q, long long t, unsigned long long* wait) {
+    if (t <= fin[q]) return;
+    long long t0 = 0;
+    for (int spin = 0;; ++spin) {
+      const int nn = vload(&cnt[q]);
+      const long long last = nn > 0 ? vload(&base[(size_t)q * M + nn - 1]) : kNegMP;
+      const bool d = vload(&done[q]) != 0;
+      const int nf = d ? vload(&cnt[q]) : nn;
+      if (last >= t || d) {
+        n[q] = nf;
+        fin[q] = d ? kEndCur : last;
+        if (val[q] == kEndCur && idx[q] < nf) val[q] = vload(&base[(size_t)q * M + idx[q]]);
+        if (spin > 0) atomicAdd(wait, (unsigned long long)(clock64() - t0));
+        return;
+      }
+      if (spin == 0) t0 = clock64();
+      __nanosleep(20);
+    }
+  }
+  __device__ __forceinline__ void advance(int q, long long len, long long t) {
+    while (val[q] + len <= t) {
+      ++idx[q];
+      val[q] = idx[q] < n[q] ? vload(&base[(size_t)q * M + idx[q]]) : kEndCur;
+    }
+  }
+  // free_at(x, x + len) fails (moves cursors only past entries ending <= x)
+  __device__ __forceinline__ bool conflict(long long own, long long len, long long x,
+                                           unsigned long long* wait) {
+    if (len <= 0) return false;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      if (q >= p) break;
+      ensure(q, x, wait);
+      advance(q, len, x);
+      if (val[q] < x + len) return true;
+    }
+    return own + len > x;
+  }
+  // earliest_fit(x, len) over the union and the own tail
+  __device__ __forceinline__ long long fit(long long own, long long len, long long x,
+                                           unsigned long long* wait) {
+    if (len <= 0) return x;
+    long long t = x;
+    for (;;) {
+      bool moved = false;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        if (q >= p) break;
+        ensure(q, t, wait);
+        advance(q, len, t);
+        while (val[q] < t + len) {
+          t = val[q] + len;
+          moved = true;
+          ensure(q, t, wait);
+          advance(q, len, t);
+        }
+      }
+      if (own + len > t) {
+        t = own + len;
         moved = true;
       }
+      if (!moved) return t;
     }
-    if (own + len > t) {
-      t = own + len;
-      moved = true;
-    }
-    if (!moved) return t;
   }
-}
-
-// free_at(x, x+len) on the same union: waits as wave_fit, but moves the
-// cursors only past reservations ending at or before x (a later wave_fit from
-// x must still see everything overlapping [x, ...))
-__device__ bool wave_conflict(WaveState& W, const long long* base, int M, const int* cnt,
-                              int* cur, int p, long long own, long long len, long long x) {
-  if (len <= 0) return false;
-  for (int q = 0; q < p; ++q) {
-    const long long* L = base + (size_t)q * M;
-    const int n = wave_wait(W, L, cnt, q, p, x);
-    int c = cur[q];
-    while (c < n && vload(&L[c]) + len <= x) ++c;
-    cur[q] = c;
-    if (c < n && vload(&L[c]) < x + len) return true;
-  }
-  return own + len > x;
-}
+};
 
 // gradient-link policy of the cascade (B = 1: the lane's one stage)
 struct WaveLinks {
   AtlasMem& X;
   WaveState& W;
-  int C, M, p, w;
+  WaveView<kWaveRegC - 1> v;
+  int C, M, w;
   long long len, own;
   __device__ __forceinline__ long long fit(int, long long y) {
-    return wave_fit(W, X.resb + (size_t)w * C * M, M, W.cnt_b[w], W.cur_b[p][w], p, own, len, y);
+    return v.fit(own, len, y, &W.wait_cyc[v.p]);
   }
   __device__ __forceinline__ bool conflict(int, long long y) {
-    return wave_conflict(W, X.resb + (size_t)w * C * M, M, W.cnt_b[w], W.cur_b[p][w], p, own, len,
-                         y);
+    return v.conflict(own, len, y, &W.wait_cyc[v.p]);
   }
   __device__ __forceinline__ void reserve(int, int pp, int k, long long e) {
     X.resb[((size_t)w * C + pp) * M + k] = e;
@@ -1219,10 +1248,12 @@ __device__ void atlas_wave_forward(const Geom& g, int mem_limit, AtlasMem& X, Wa
   long long gfr[1] = {0};
   int drr[1] = {0};
   long long n0 = 0, n1 = 0, n2 = 0;
-  WaveLinks links{X, W, C, M, p, wbi[0] >= 0 ? wbi[0] : 0, serb[0], kNegMP};
-  if (wbi[0] < 0) links.len = 0;
-  for (int q = 0; q < kWaveMaxC; ++q)
-    for (int w = lane; w < nw; w += 32) W.cur_f[p][w][q] = W.cur_b[p][w][q] = 0;
+  const int wb = wbi[0] >= 0 ? wbi[0] : 0;
+  WaveLinks links{X, W, {}, C, M, wb, wbi[0] >= 0 ? serb[0] : 0, kNegMP};
+  links.v.init(X.resb + (size_t)wb * C * M, W.cnt_b[wb], W.done, M, p);
+  const int wf = lane < nw ? lane : 0;  // lane w < nw: forward link w
+  WaveView<kWaveRegC - 1> fv;
+  fv.init(X.resf + (size_t)wf * C * M, W.cnt_f[wf], W.done, M, p);
   long long aw_l = 0, lenw_l = 0, ownw_l = kNegMP;
   if (lane < nw) {
     aw_l = X.wa[lane];
@@ -1244,16 +1275,12 @@ __device__ void atlas_wave_forward(const Geom& g, int mem_limit, AtlasMem& X, Wa
     if (nw > 0) {
       for (;;) {
         const long long e = aw_l + f + imax(t0, gw);
-        const bool conf = lane < nw && wave_conflict(W, X.resf + (size_t)lane * C * M, M,
-                                                     W.cnt_f[lane], W.cur_f[p][lane], p, ownw_l,
-                                                     lenw_l, e);
+        const bool conf = lane < nw && fv.conflict(ownw_l, lenw_l, e, &W.wait_cyc[p]);
         const unsigned bal = __ballot_sync(kFull, conf);
         if (!bal) break;
         const int src = __ffs(bal) - 1;  // the lowest conflicting link shifts t0
         long long shift = 0;
-        if (lane == src)
-          shift = wave_fit(W, X.resf + (size_t)lane * C * M, M, W.cnt_f[lane], W.cur_f[p][lane],
-                           p, ownw_l, lenw_l, e) - e;
+        if (lane == src) shift = fv.fit(ownw_l, lenw_l, e, &W.wait_cyc[p]) - e;
         t0 += shfl_idx64(shift, src);
       }
       if (lane < nw) {
