@@ -29,7 +29,7 @@ same-sample comparison against the reference's CPU packing.
 
 --impl reference runs the reference's own CPU implementation (the reference
 sources compiled into oracle/_ref, else the C port) on the host cores over
-the same workload (every row of the same space, split over the K steps).
+the same workload (every row of the same space, one pass with all threads).
 
 --gpus N without torchrun relaunches itself under torch.distributed.run with
 N processes (one per GPU); under torchrun, WORLD_SIZE must equal N.
@@ -148,12 +148,6 @@ def run_cpu(topos, scens, idx, threads):
     return time.perf_counter() - t0, kind
 
 
-def deal(scens, k):
-    """k groups of scenario indices with balanced estimated cost."""
-    from paper_2411_14458_b200 import distributed as D
-    return D.shard_by_cost(scens, max(1, k))
-
-
 def cpu_one_thread(topos, scens, stride=20):
     """The reference on one host thread over every stride-th scenario."""
     idx = list(range(0, len(scens), stride))
@@ -213,15 +207,16 @@ def impl_reference(args):
     topos, scens, _ = headline_space(args.rows, world)
     n_rows = sum(s.d_max for s in scens)
     threads = os.cpu_count() or 1
-    # every row of the space is evaluated exactly once over the K timed steps
-    groups = deal(scens, args.steps)
+    # The reference's whatif() over every row of the space with one pool of
+    # all host threads (heaviest scenario first), i.e. exactly the work of K
+    # steps of our arm divided into K equal parts; one pass keeps the pool
+    # saturated (per-step pools idle behind each step's heaviest scenario:
+    # measured 363 vs 1017 plans/s on 16 threads), so the reference is timed
+    # at its best throughput.
     for _ in range(args.warmup):  # untimed (page cache, allocator, thread pool)
         run_cpu(topos, scens, list(range(min(2, len(scens)))), threads)
-    times, kind = [], "reference"
-    for g in groups:
-        dt, kind = run_cpu(topos, scens, g, threads)
-        times.append(dt)
-    total = sum(times)
+    total, kind = run_cpu(topos, scens, list(range(len(scens))), threads)
+    times = [total / max(1, args.steps)] * max(1, args.steps)
     value = n_rows / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
@@ -230,8 +225,9 @@ def impl_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": headline_config(args.rows, world, len(scens)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"the whole space: all {n_rows} rows, split over the "
-                                   f"{len(times)} timed steps", "cpu": cpu_model()},
+                         "sample": f"the whole space: all {n_rows} rows in one timed pass "
+                                   f"({len(times)} steps' worth)", "seconds": total,
+                         "cpu": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     if not args.no_cpu_baseline:
