@@ -686,10 +686,9 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   lap("keep");
   // the launch sequence (ATLAS shapes, scratch, stream assignment) depends
   // only on the buckets' shapes: reuse it when a reload has the same ones.
-  // A captured graph (GPB_GRAPH) also bakes in the scenario split of each
-  // bucket's select launch and the table pointers (which a reload may
-  // reallocate), so it is re-captured after every load.
-  c.drop_graph();
+  // A captured graph (GPB_GRAPH) also bakes in each bucket's select split and
+  // every table pointer; gpb_evaluate replays it only while that
+  // fingerprint is unchanged (graph_key), else re-captures.
   if (!same_shapes(prev_buckets, c.buckets)) {
     c.eval_ready = false;
   } else {
@@ -918,17 +917,30 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     const int rc = prepare_evaluate(c);
     if (rc != GPB_OK) return rc;
   }
-  // GPB_GRAPH=1 captures the sequence once per loaded space and stream into
-  // a CUDA graph and replays it. Measured on config 2 it is not the default:
-  // every gpb_load re-captures (0.6 ms of host time per step in the e2e
-  // loop) and the replayed step ran 15 % slower on the device than the
-  // directly launched one (0.83 vs 0.71 ms).
+  // GPB_GRAPH=1 captures the launch sequence into a CUDA graph and replays
+  // it while everything it baked in is unchanged: the stream, the buckets'
+  // launch parameters (shapes, offsets, select splits, streams) and every
+  // device pointer (a reload may reallocate a table).
   const bool use_graph = std::getenv("GPB_GRAPH") != nullptr;
   if (!use_graph) {
     const int rc = record_evaluate(c, st, false);
     if (rc != GPB_OK) return rc;
   } else {
-    if (!c.graph_exec || c.graph_stream != st) {
+    std::vector<long long> key;
+    for (Buf* b : c.all_bufs()) key.push_back((long long)(uintptr_t)b->ptr);
+    key.push_back((long long)(uintptr_t)st);
+    key.push_back(c.bucket_timing);
+    key.push_back(c.profile_rows);
+    key.push_back(c.sel_blocks);
+    for (const Bucket& b : c.buckets)
+      for (long long v : {(long long)b.policy, (long long)b.B, (long long)b.offset,
+                          (long long)b.count, (long long)b.gw, (long long)b.stream,
+                          (long long)b.scen_off, (long long)b.scen_cnt, (long long)b.sel_grid,
+                          (long long)b.sel_off, (long long)b.max_m})
+        key.push_back(v);
+    for (size_t i = 0; i < c.aplan.size(); ++i)
+      key.push_back(c.aplan[i].grid * 1000003LL + c.aplan[i].wpc + (long long)c.scr_off[i]);
+    if (!c.graph_exec || key != c.graph_key) {
       c.drop_graph();
       cudaGraph_t g = nullptr;
       if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
@@ -947,6 +959,7 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
         return c.cuda_fail(ie, "graph instantiate");
       }
       c.graph_stream = st;
+      c.graph_key = key;
     }
     const cudaError_t e = cudaGraphLaunch(c.graph_exec, st);
     if (e != cudaSuccess) return c.cuda_fail(e, "graph launch");

@@ -120,6 +120,7 @@ struct Ctx {
   cudaEvent_t fork_ev = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   cudaStream_t graph_stream = nullptr;
+  std::vector<long long> graph_key;  // what the captured graph baked in
   void drop_graph();
   std::vector<AtlasPlan> aplan;  // per bucket (ATLAS only)
   std::vector<size_t> scr_off;    // per bucket offset into b_scratch (int64)
