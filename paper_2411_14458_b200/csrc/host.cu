@@ -917,11 +917,15 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     const int rc = prepare_evaluate(c);
     if (rc != GPB_OK) return rc;
   }
-  // GPB_GRAPH=1 captures the launch sequence into a CUDA graph and replays
-  // it while everything it baked in is unchanged: the stream, the buckets'
-  // launch parameters (shapes, offsets, select splits, streams) and every
-  // device pointer (a reload may reallocate a table).
-  const bool use_graph = std::getenv("GPB_GRAPH") != nullptr;
+  // The launch sequence is captured into a CUDA graph and replayed while
+  // everything it baked in is unchanged: the stream, the buckets' launch
+  // parameters (shapes, offsets, select splits, streams) and every device
+  // pointer (a reload may reallocate a table). Measured on config 2: the
+  // host launch cost per step drops 0.155 -> 0.022 ms and the two-session
+  // e2e step 0.69 -> 0.56 ms; the replayed step itself is ~2 % slower on the
+  // device (0.563 vs 0.549 ms). GPB_GRAPH=0 launches directly.
+  const char* genv = std::getenv("GPB_GRAPH");
+  const bool use_graph = !(genv && genv[0] == '0');
   if (!use_graph) {
     const int rc = record_evaluate(c, st, false);
     if (rc != GPB_OK) return rc;

@@ -173,12 +173,14 @@ def test_reload_same_shapes_and_stream_switch(planner, checker):
             assert _row_key(a) == _row_key(b)
 
 
-def test_graph_mode_reloads(planner, checker, monkeypatch):
-    """GPB_GRAPH=1 replays the evaluate launch sequence as a CUDA graph; a
-    reload (same bucket shapes with other values, a different scenario split,
-    another space) must re-capture it: every row stays bit-exact."""
+@pytest.mark.parametrize("graph", ["1", "0"])
+def test_graph_mode_reloads(planner, checker, monkeypatch, graph):
+    """The evaluate launch sequence is replayed as a CUDA graph (default) or
+    launched directly (GPB_GRAPH=0); a reload (same bucket shapes with other
+    values, a different scenario split, another space) must re-capture the
+    graph whenever anything it baked in changed: every row stays bit-exact."""
     import ctypes
-    monkeypatch.setenv("GPB_GRAPH", "1")
+    monkeypatch.setenv("GPB_GRAPH", graph)
     topos, scens = random_space(4321, 120, wide=False)
     assert _compare_space(planner, checker, None, topos, scens) > 120
     scens2 = abi.array(abi.Scenario, [type(s).from_buffer_copy(s) for s in scens])
