@@ -263,6 +263,12 @@ int gpb_saturating_requests(gpb_ctx* ctx, int64_t row, const gpb_prefill_model* 
 int gpb_validate_timeline(gpb_ctx* ctx, int64_t row, const int64_t* fe, const int64_t* ps,
                           int32_t* check, int64_t* where);
 
+/* append_allreduce (scheduler.cpp:613-650) of one row computed on the device:
+ * per stage s < *n_stages, the start (last backward end over every replica)
+ * and duration of its all-reduce task; written when cap >= *n_stages. */
+int gpb_allreduce_tail(gpb_ctx* ctx, int64_t row, int64_t* start_ns, int64_t* dur_ns,
+                       int32_t cap, int32_t* n_stages);
+
 /* Deterministic request sources on the host (bubbletea.cpp:269-284). */
 int gpb_synthetic_requests(int32_t count, uint32_t seed, double horizon_ms,
                            const gpb_prefill_model* pm, gpb_request* out);

@@ -64,6 +64,9 @@ class Checker:
             self._whatif = f("whatif_count", C.c_int,
                              [P(abi.Topology), P(abi.Scenario), C.c_int32,
                               P(C.c_int64), P(C.c_int64)])
+            self._artail = f("allreduce_tail", C.c_int,
+                             [P(abi.Topology), P(abi.Scenario), C.c_int32, P(C.c_int64),
+                              P(C.c_int64), C.c_int32, P(C.c_int32)])
             self._report = f("report_rows", C.c_int,
                              [P(abi.Topology), P(abi.Scenario), C.c_int32,
                               P(C.c_double), P(C.c_int64)])
@@ -160,6 +163,14 @@ class Checker:
         mk = (C.c_int64 * max(1, n))()
         self._check(self._report(topos, C.byref(sc), n, util, mk))
         return list(zip(util[:n], mk[:n]))
+
+    def allreduce_tail(self, topos, sc, d):
+        """[(start_ns, duration_ns)] per stage of append_allreduce
+        (scheduler.cpp:613-650) on row d's schedule (reference only)."""
+        cap = 512
+        st, du, n = (C.c_int64 * cap)(), (C.c_int64 * cap)(), C.c_int32()
+        self._check(self._artail(topos, C.byref(sc), d, st, du, cap, C.byref(n)))
+        return list(zip(st[:n.value], du[:n.value]))
 
     def whatif_count(self, topos, scens):
         arr = abi.array(abi.Scenario, scens)

@@ -271,6 +271,28 @@ int ref_report_rows(const gpb_topology* topos, const gpb_scenario* sc,
   });
 }
 
+// append_allreduce (scheduler.cpp:613-650) on the schedule of row d: per
+// stage the start and duration of its all-reduce task (cell 0, pipeline 0).
+int ref_allreduce_tail(const gpb_topology* topos, const gpb_scenario* sc, int32_t d,
+                       int64_t* start, int64_t* dur, int32_t cap, int32_t* n_stages) {
+  return guarded([&] {
+    SelectionInput in = to_input(topos, *sc);
+    ParallelismPlan plan = build_plan(in.topo, in.model, d, in.pipelines_per_cell,
+                                      in.dc_order, in.tp_degree);
+    ComputeProfile prof = resolved_profile(in);
+    Schedule sched = schedule_for_policy(in.policy, plan, in.model, prof, in.topo, in.sched);
+    sched = append_allreduce(sched, plan, in.model, in.topo);
+    const int S = plan.num_stages();
+    *n_stages = S;
+    for (const ScheduledTask& t : sched.tasks)
+      if (t.kind == TaskKind::AllReduce && t.cell_id == 0 && t.pipeline_id == 0 &&
+          t.stage < cap) {
+        start[t.stage] = t.start;
+        dur[t.stage] = t.end - t.start;
+      }
+  });
+}
+
 int ref_bubbles(const gpb_topology* topos, const gpb_scenario* sc, int32_t d,
                 int64_t horizon, gpb_bubble* out, int64_t cap, int64_t* n) {
   return guarded([&] {

@@ -48,6 +48,32 @@ struct TlSlot {
   int S, M, Ce, C, D, policy;
 };
 
+// append_allreduce's task durations (scheduler.cpp:613-650): per stage,
+// allreduce_time_ms (comm_model.cpp:38-41) of the stage's parameters over the
+// D*C replicas at its DC's intra bandwidth, the same double operations as
+// finish_row, rounded by ms_to_ns. One block per slot, threads over stages.
+__global__ void ar_dur_kernel(const TlSlot* slots, int n_slots, const DevScen* scens,
+                              const DevTopo* topos, const int32_t* row_scen, long long* ar_dur) {
+  const int si = blockIdx.x;
+  if (si >= n_slots) return;
+  const TlSlot& sl = slots[si];
+  if (sl.ar_off < 0) return;
+  const DevScen& sc = scens[row_scen[sl.row]];
+  const DevTopo& tp = topos[sc.topo];
+  Geom g;
+  decode(sc, tp, sl.D, g);
+  const int n = sl.D * sc.C;
+  for (int s = threadIdx.x; s < sl.S; s += blockDim.x) {
+    const int begin = s * sc.lpp, end = min(begin + sc.lpp, sc.L);
+    const double params = __dmul_rn(sc.ppl, (double)max(0, end - begin));
+    double ms = 0.0;
+    if (n > 1)
+      ms = __ddiv_rn(__dmul_rn(__dmul_rn(4.0, params), (double)(n - 1)),
+                     __dmul_rn((double)n, tp.intra_bw[g.blk_dc[block_of(g, s)]]));
+    ar_dur[sl.ar_off + s] = ms_to_ns(ms);
+  }
+}
+
 // Horizon per slot: the given one, else the makespan of the timeline incl.
 // the optional all-reduce tail (append_allreduce, scheduler.cpp:613-650:
 // each stage's all-reduce starts at the stage's last backward end over all
@@ -1054,7 +1080,7 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
   cudaStream_t st = c.stream;
   slots.resize(n);
   long long tl = 0, gp = 0, ls = 0;
-  std::vector<long long> ar_host;
+  long long n_ar = 0;
   for (int i = 0; i < n; ++i) {
     if (rows[i] < 0 || rows[i] >= c.n_rows) {
       c.set_error("row index out of range");
@@ -1084,18 +1110,9 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
     s.gap_off = gp;
     s.lst_off = ls;
     s.ar_off = -1;
-    if (with_allreduce) {
-      // allreduce_time_ms per stage (comm_model.cpp:38-41) -> ms_to_ns
-      s.ar_off = (long long)ar_host.size();
-      const int N = d * sc.C;
-      for (int st2 = 0; st2 < sc.S; ++st2) {
-        int b = 0;
-        while (b + 1 < hb.nb && st2 >= hb.first[b + 1]) ++b;
-        const int begin = st2 * sc.lpp, end = std::min(begin + sc.lpp, sc.L);
-        const double params = sc.ppl * std::max(0, end - begin);
-        const double ms = N <= 1 ? 0.0 : 4.0 * params * (N - 1) / (N * tp.intra_bw[hb.dc[b]]);
-        ar_host.push_back(host_ms_to_ns(ms));
-      }
+    if (with_allreduce) {  // per-stage tail durations: ar_dur_kernel, on the device
+      s.ar_off = n_ar;
+      n_ar += sc.S;
     }
     tl += (long long)s.Ce * s.S * s.M;
     gp += (long long)s.Ce * s.S * (2 * s.M + 1);
@@ -1186,11 +1203,14 @@ int build_timelines(Ctx& c, const int64_t* rows, int n, long long horizon,
     }
     if (e != cudaSuccess) return c.cuda_fail(e, "timeline launch");
   }
-  long long* ar_dev = (long long*)c.dev_buf(c.b_ar, 16 * std::max<size_t>(1, ar_host.size()));
+  long long* ar_dev = (long long*)c.dev_buf(c.b_ar, 16 * std::max<size_t>(1, n_ar));
   if (!ar_dev) return c.cuda_fail(cudaErrorMemoryAllocation, "allreduce buffers");
-  long long* ar_start = ar_dev + std::max<size_t>(1, ar_host.size());
-  if (!ar_host.empty())
-    cudaMemcpyAsync(ar_dev, ar_host.data(), 8 * ar_host.size(), cudaMemcpyHostToDevice, st);
+  long long* ar_start = ar_dev + std::max<long long>(1, n_ar);
+  if (n_ar > 0)
+    ar_dur_kernel<<<n, 128, 0, st>>>(dslots, n, (const DevScen*)c.b_scens.ptr,
+                                     (const DevTopo*)c.b_topos.ptr,
+                                     (const int32_t*)c.b_row_scen.ptr, ar_dev);
+  c.tl_ar = ar_dev;
   cudaMemsetAsync(hz, 0, 8 * (size_t)n, st);
   horizon_kernel<<<n, 128, 0, st>>>(dslots, n, tl_rows, ps, ar_dev, ar_start, hz);
   long long max_lists = 1;
@@ -1943,6 +1963,33 @@ extern "C" int gpb_validate_timeline(gpb_ctx* ctx_, int64_t row, const int64_t* 
   } else {
     *check = 0;
     if (where) *where = 0;
+  }
+  return GPB_OK;
+}
+
+// append_allreduce (scheduler.cpp:613-650) of one row from the device: each
+// stage's all-reduce starts at the stage's last backward end over every
+// replica (horizon_kernel) and lasts ar_dur_kernel's duration.
+extern "C" int gpb_allreduce_tail(gpb_ctx* ctx_, int64_t row, int64_t* start_ns, int64_t* dur_ns,
+                                  int32_t cap, int32_t* n_stages) {
+  if (!ctx_ || !n_stages) return GPB_ERROR;
+  Ctx& c = *reinterpret_cast<Ctx*>(ctx_);
+  c.last_error.clear();
+  if (!c.loaded) {
+    c.set_error("no plan space loaded");
+    return GPB_CONFIG_ERROR;
+  }
+  cudaSetDevice(c.device);
+  std::vector<TlSlot> slots;
+  int rc = build_timelines(c, &row, 1, 0, slots, true);
+  if (rc != GPB_OK) return rc;
+  const int S = slots[0].S;
+  *n_stages = S;
+  if (start_ns && dur_ns && cap >= S) {
+    cudaMemcpyAsync(dur_ns, c.tl_ar, 8 * (size_t)S, cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(start_ns, c.tl_ar + S, 8 * (size_t)S, cudaMemcpyDeviceToHost, c.stream);
+    const cudaError_t e = cudaStreamSynchronize(c.stream);
+    if (e != cudaSuccess) return c.cuda_fail(e, "allreduce tail");
   }
   return GPB_OK;
 }

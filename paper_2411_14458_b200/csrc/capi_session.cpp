@@ -778,29 +778,25 @@ Timeline device_timeline(Session& se, const RunConfig& c, const std::string& pol
   return t;
 }
 
-// append_allreduce (scheduler.cpp:613-650)
-void append_allreduce(Timeline& t, const RunConfig& c, const PlanInfo& plan) {
-  const int N = plan.D * plan.C;
-  std::vector<long long> last(plan.S, 0);
-  for (const Task& x : t.tasks)
-    if (x.kind == kBackward) last[x.stage] = std::max(last[x.stage], x.end);
-  for (int s = 0; s < plan.S; ++s) {
-    const int begin = s * c.model.lpp, end = std::min(begin + c.model.lpp, c.model.num_layers);
-    const double params = c.model.ppl() * std::max(0, end - begin);
-    const double bw = c.topo.dcs[plan.stage_dc[s]].intra_bw;
-    const double ms = N <= 1 ? 0.0 : 4.0 * params * (N - 1) / (N * bw);
-    const long long dur = ms_to_ns(ms);
+// append_allreduce (scheduler.cpp:613-650): the tail's starts and durations
+// come from the device (gpb_allreduce_tail on the row device_timeline loaded)
+void append_allreduce(Session& se, Timeline& t, const RunConfig& c, const PlanInfo& plan) {
+  std::vector<int64_t> start(plan.S), dur(plan.S);
+  int32_t n = 0;
+  se.check(gpb_allreduce_tail(se.device(), c.dp_cells - 1, start.data(), dur.data(),
+                              (int32_t)plan.S, &n));
+  if (n != plan.S) throw Internal("all-reduce tail: stage count mismatch");
+  for (int s = 0; s < plan.S; ++s)
     for (int cell = 0; cell < plan.D; ++cell)
       for (int p = 0; p < plan.C; ++p)
         t.tasks.push_back({plan.gpu[((size_t)cell * plan.C + p) * plan.S + s], cell, p, kAllReduce,
-                           0, s, last[s], last[s] + dur});
-  }
+                           0, s, start[s], start[s] + dur[s]});
   finalize(t);
 }
 
 Timeline simulate(Session& se, const RunConfig& c, const std::string& policy, PlanInfo& plan) {
   Timeline t = device_timeline(se, c, policy, plan);
-  if (c.with_allreduce) append_allreduce(t, c, plan);
+  if (c.with_allreduce) append_allreduce(se, t, c, plan);
   return t;  // run(): the replay reproduces the schedule (test_engine.cpp:17-32)
 }
 

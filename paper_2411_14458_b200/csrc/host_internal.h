@@ -109,6 +109,7 @@ struct Ctx {
   long long *tl_glo = nullptr, *tl_ghi = nullptr, *tl_gsum = nullptr, *tl_hz = nullptr;
   unsigned char* tl_gfl = nullptr;
   longlong2* tl_gpk = nullptr;  // packed copy of the gap lists (pack kernel)
+  long long* tl_ar = nullptr;   // all-reduce tail: durations [n_ar], then starts [n_ar]
   int *tl_gcnt = nullptr, *tl_ghas = nullptr;
   void* tl_slots_dev = nullptr;
   bool timing_valid = false;

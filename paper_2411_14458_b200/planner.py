@@ -89,6 +89,8 @@ def load_library(path: str = LIB_PATH):
                                               P(C.c_int64)]),
         "gpb_validate_timeline": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_int64), P(C.c_int64),
                                             P(C.c_int32), P(C.c_int64)]),
+        "gpb_allreduce_tail": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_int64), P(C.c_int64),
+                                         C.c_int32, P(C.c_int32)]),
         "gpb_group_create": (C.c_void_p, [C.c_int32, P(C.c_int32)]),
         "gpb_group_destroy": (None, [C.c_void_p]),
         "gpb_group_last_error": (C.c_char_p, [C.c_void_p]),
@@ -116,6 +118,7 @@ def exported_symbols():
             "gpb_copy_best", "gpb_set_profile", "gpb_fetch_row_cycles",
             "gpb_set_allreduce_tail", "gpb_timeline_arrays", "gpb_bucket_infos",
             "gpb_set_bucket_timing", "gpb_saturating_requests", "gpb_validate_timeline",
+            "gpb_allreduce_tail",
             "gpb_group_create", "gpb_group_destroy",
             "gpb_group_last_error", "gpb_group_size", "gpb_group_load", "gpb_group_evaluate",
             "gpb_group_fetch_rows", "gpb_group_fetch_scenarios", "gpb_group_fetch_best"]
@@ -273,6 +276,15 @@ class Planner:
         fe, ps = (C.c_int64 * n)(), (C.c_int64 * n)()
         self._check(self.lib.gpb_timeline_arrays(self.ctx, row, fe, ps, n, dims, C.byref(mk)))
         return fe, ps, tuple(dims), mk.value
+
+    def allreduce_tail(self, row: int):
+        """append_allreduce (scheduler.cpp:613-650) on the device: per stage
+        (start_ns, duration_ns) of the all-reduce task."""
+        n = C.c_int32()
+        self._check(self.lib.gpb_allreduce_tail(self.ctx, row, None, None, 0, C.byref(n)))
+        st, du = (C.c_int64 * max(1, n.value))(), (C.c_int64 * max(1, n.value))()
+        self._check(self.lib.gpb_allreduce_tail(self.ctx, row, st, du, n.value, C.byref(n)))
+        return list(zip(st[:n.value], du[:n.value]))
 
     def validate(self, row: int, fe=None, ps=None):
         """validate_timeline (validate.h:77-256) on the device: (check, where)."""

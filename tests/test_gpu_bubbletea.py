@@ -228,3 +228,23 @@ def test_saturating_requests_on_device(planner, checker, wide):
     got = [(q.id, q.arrival_ms, q.tokens) for q in planner.saturating_requests(0, pm)]
     assert got == [(q.id, q.arrival_ms, q.tokens) for q in checker.saturating(topos, sc, 1, pm)]
     assert len(got) > 10
+
+
+def test_allreduce_tail_on_device(planner, checker):
+    """append_allreduce (scheduler.cpp:613-650) computed on the device: every
+    stage's all-reduce start (the last backward end over all replicas) and
+    duration equal the reference's on random spaces of every policy."""
+    if not hasattr(checker, "allreduce_tail"):
+        pytest.skip("needs the compiled reference (oracle/_ref)")
+    for wide in (False, True):
+        topos, scens = random_space(61 if wide else 62, 100, wide)
+        rng = random.Random(6)
+        n = 0
+        for i, r in _feasible_rows(planner, topos, scens, limit_gpus=3000):
+            if rng.random() > 0.3:
+                continue
+            sc = scens[r.scenario]
+            assert planner.allreduce_tail(i) == checker.allreduce_tail(topos, sc, r.d), \
+                (i, r.d, abi.POLICY_NAMES[sc.policy])
+            n += 1
+        assert n > 10
