@@ -58,6 +58,32 @@ struct SeqMem {
   __device__ __forceinline__ long long& at(long long k) const { return base[k]; }
 };
 
+// The row's small, hot scalars — per-link serialization / latency, list
+// lengths and cursors, the drain's candidates — live in shared memory, one
+// column per thread ([field][thread]: conflict-free). As local arrays they
+// were a 720-byte stack frame per thread, 368 KB per SM at 4 blocks: more
+// than L1, so every cursor step went to L2.
+constexpr int kSeqLinks = GPB_MAX_DC - 1;
+struct SeqSmall {
+  long long* l;  // [field][thread] int64: ser[7] lat[7] T.cand(8)
+  int* i;        // [field][thread] int32: nf nb ofn obn cf cb [7 each], mq cq [8 each]
+  signed char* lk;  // [16][thread]: WAN link after stage s
+  int t;
+  __device__ __forceinline__ long long& ser(int w) const { return l[(0 + w) * kEvalThreads + t]; }
+  __device__ __forceinline__ long long& lat(int w) const { return l[(7 + w) * kEvalThreads + t]; }
+  __device__ __forceinline__ long long& cand(int q) const { return l[(14 + q) * kEvalThreads + t]; }
+  __device__ __forceinline__ int& nf(int w) const { return i[(0 + w) * kEvalThreads + t]; }
+  __device__ __forceinline__ int& nb(int w) const { return i[(7 + w) * kEvalThreads + t]; }
+  __device__ __forceinline__ int& ofn(int w) const { return i[(14 + w) * kEvalThreads + t]; }
+  __device__ __forceinline__ int& obn(int w) const { return i[(21 + w) * kEvalThreads + t]; }
+  __device__ __forceinline__ int& cf(int w) const { return i[(28 + w) * kEvalThreads + t]; }
+  __device__ __forceinline__ int& cb(int w) const { return i[(35 + w) * kEvalThreads + t]; }
+  __device__ __forceinline__ int& mq(int q) const { return i[(42 + q) * kEvalThreads + t]; }
+  __device__ __forceinline__ int& cq(int q) const { return i[(50 + q) * kEvalThreads + t]; }
+  __device__ __forceinline__ signed char& link(int s) const { return lk[s * kEvalThreads + t]; }
+};
+constexpr int kSeqSmallBytes = (22 * 8 + 58 * 4 + 16) * kEvalThreads;
+
 // ring slots for a row: the smallest power of two >= min(mem_limit, M)
 __host__ __device__ __forceinline__ int seq_ring(int L, int M) {
   const int n = L < M ? L : M;
@@ -137,7 +163,7 @@ __device__ __forceinline__ int link_of(const Geom& g, int s) {
 // stage loops, which are unrolled so the current pipeline's per-stage state
 // (gpu_free, drained counts, WAN links) stays in registers.
 template <int SMAX>
-__device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
+__device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X, const SeqSmall& T) {
   const int S = g.S, M = g.M, C = g.C;
   const long long f = g.fwd, dur = g.dur;
   SeqLayout Y;
@@ -151,22 +177,25 @@ __device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
     for (int b = 1; b < g.nb; ++b)
       if (g.blk_first[b] == s + 1 && s + 1 < S) lk[s] = b - 1;
   }
-  int nf[GPB_MAX_DC], nb_[GPB_MAX_DC], of_n[GPB_MAX_DC], ob_n[GPB_MAX_DC];
-  for (int w = 0; w < nw; ++w) nf[w] = nb_[w] = of_n[w] = ob_n[w] = 0;
+  for (int w = 0; w < nw; ++w) {
+    T.nf(w) = T.nb(w) = T.ofn(w) = T.obn(w) = 0;
+    T.ser(w) = g.ser_pooled[w];
+    T.lat(w) = g.lat[w];
+  }
+  for (int s = 0; s < S; ++s) T.link(s) = (signed char)link_of(g, s);
 
   // ------------------------------------------------------ forward phase
   for (int p = 0; p < C; ++p) {
     if (p > 0) {  // fold pipeline p-1's lists into the static ones
       for (int w = 0; w < nw; ++w) {
-        merge_into(X, Y.mf(w), nf[w], Y.of(w), of_n[w]);
-        nf[w] += of_n[w];
-        merge_into(X, Y.mb(w), nb_[w], Y.ob(w), ob_n[w]);
-        nb_[w] += ob_n[w];
-        of_n[w] = ob_n[w] = 0;
+        merge_into(X, Y.mf(w), T.nf(w), Y.of(w), T.ofn(w));
+        T.nf(w) += T.ofn(w);
+        merge_into(X, Y.mb(w), T.nb(w), Y.ob(w), T.obn(w));
+        T.nb(w) += T.obn(w);
+        T.ofn(w) = T.obn(w) = 0;
       }
     }
-    int cf[GPB_MAX_DC], cb[GPB_MAX_DC];
-    for (int w = 0; w < nw; ++w) cf[w] = cb[w] = 0;
+    for (int w = 0; w < nw; ++w) T.cf(w) = T.cb(w) = 0;
     long long gfr[SMAX];
     int drr[SMAX];
 #pragma unroll
@@ -193,18 +222,18 @@ __device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
           if (s >= S || s < s_min) continue;
           const int upto = s == s_min ? m - L + 1 : m;
           const int w = s > 0 ? lk[s - 1] : -1;
-          const long long len = w >= 0 ? g.ser_pooled[w] : 0;
-          const long long wl = w >= 0 ? len + g.lat[w] : 0;
+          const long long len = w >= 0 ? T.ser(w) : 0;
+          const long long wl = w >= 0 ? len + T.lat(w) : 0;
           long long gv = gfr[s];
           for (int mm = drr[s]; mm < upto; ++mm) {
             const long long ready =
                 s == S - 1 ? X.at(fdlp + (mm & RM)) : X.at(gap + (long long)s * R + (mm & RM));
             long long t = imax(ready, gv);
             if (len > 0) {  // atlas_pair_start (:287-294) + reserve
-              const long long own = ob_n[w] > 0 ? X.at(Y.ob(w) + ob_n[w] - 1) : kNegInf;
-              t = fit(X, Y.mb(w), nb_[w], cb[w], own, len, t + dur) - dur;
-              X.at(Y.ob(w) + ob_n[w]) = t + dur;
-              ++ob_n[w];
+              const long long own = T.obn(w) > 0 ? X.at(Y.ob(w) + T.obn(w) - 1) : kNegInf;
+              t = fit(X, Y.mb(w), T.nb(w), T.cb(w), own, len, t + dur) - dur;
+              X.at(Y.ob(w) + T.obn(w)) = t + dur;
+              ++T.obn(w);
             }
             gv = t + dur;  // atlas_commit_pair (:298-317)
             if (s > 0) X.at(gap + (long long)(s - 1) * R + (mm & RM)) = gv + wl;
@@ -228,16 +257,16 @@ __device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
             const int w = lk[s];
             cur = e;
             if (w >= 0) {
-              const long long len = g.ser_pooled[w];
+              const long long len = T.ser(w);
               if (len > 0) {
-                const long long own = of_n[w] > 0 ? X.at(Y.of(w) + of_n[w] - 1) : kNegInf;
-                const long long slot = fit(X, Y.mf(w), nf[w], cf[w], own, len, e);
+                const long long own = T.ofn(w) > 0 ? X.at(Y.of(w) + T.ofn(w) - 1) : kNegInf;
+                const long long slot = fit(X, Y.mf(w), T.nf(w), T.cf(w), own, len, e);
                 if (slot != e) {
                   t0 += slot - e;
                   ok = false;
                 }
               }
-              cur = e + len + g.lat[w];
+              cur = e + len + T.lat(w);
             }
           }
         }
@@ -252,11 +281,11 @@ __device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
           cur = e;
           const int w = lk[s];
           if (w >= 0) {
-            if (g.ser_pooled[w] > 0) {
-              X.at(Y.of(w) + of_n[w]) = e;
-              ++of_n[w];
+            if (T.ser(w) > 0) {
+              X.at(Y.of(w) + T.ofn(w)) = e;
+              ++T.ofn(w);
             }
-            cur = e + g.ser_pooled[w] + g.lat[w];
+            cur = e + T.ser(w) + T.lat(w);
           }
           if (s == S - 1) X.at(fdlp + (m & RM)) = e;
         }
@@ -271,17 +300,17 @@ __device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
   }
   // the last pipeline's forced drains join the static gradient lists
   for (int w = 0; w < nw; ++w) {
-    merge_into(X, Y.mb(w), nb_[w], Y.ob(w), ob_n[w]);
-    nb_[w] += ob_n[w];
+    merge_into(X, Y.mb(w), T.nb(w), Y.ob(w), T.obn(w));
+    T.nb(w) += T.obn(w);
   }
 
   // ------------------------------------------- drain: stage by stage
   long long mk = 0;
   for (int s = S - 1; s >= 0; --s) {
-    const int w = s > 0 ? link_of(g, s - 1) : -1;
-    const long long len = w >= 0 ? g.ser_pooled[w] : 0;
+    const int w = s > 0 ? (int)T.link(s - 1) : -1;
+    const long long len = w >= 0 ? T.ser(w) : 0;
     if (w < 0 || len <= 0) {  // no shared resource: e[m] = max(r[m], e[m-1]) + dur
-      const long long wl2 = w >= 0 ? g.lat[w] : 0;  // len == 0 WAN stage: latency only
+      const long long wl2 = w >= 0 ? T.lat(w) : 0;  // len == 0 WAN stage: latency only
       for (int p = 0; p < C; ++p) {
         long long gfv = X.at(Y.gf + (long long)p * S + s);
         for (int m = (int)X.at(Y.dr + (long long)p * S + s); m < M; ++m) {
@@ -296,44 +325,42 @@ __device__ long long atlas_seq_row(const Geom& g, int L, const SeqMem& X) {
       continue;
     }
     // WAN gradient link: greedy over the pipelines' next pairs
-    const long long wl2 = len + g.lat[w];
+    const long long wl2 = len + T.lat(w);
     long long last = kNegInf;  // start of this stage's last committed transfer
-    long long cand[kSeqMaxC];
-    int mq[kSeqMaxC], cq[kSeqMaxC];
     for (int q = 0; q < C; ++q) {
-      mq[q] = (int)X.at(Y.dr + (long long)q * S + s);
-      cq[q] = 0;
-      cand[q] = kInf64;
-      if (mq[q] < M) {
-        const long long r = s == S - 1 ? X.at(Y.fdl + (long long)q * R + (mq[q] & RM))
-                                       : X.at(Y.ga + ((long long)q * S + s) * R + (mq[q] & RM));
+      T.mq(q) = (int)X.at(Y.dr + (long long)q * S + s);
+      T.cq(q) = 0;
+      T.cand(q) = kInf64;
+      if (T.mq(q) < M) {
+        const long long r = s == S - 1 ? X.at(Y.fdl + (long long)q * R + (T.mq(q) & RM))
+                                       : X.at(Y.ga + ((long long)q * S + s) * R + (T.mq(q) & RM));
         const long long lo = imax(r, X.at(Y.gf + (long long)q * S + s));
-        cand[q] = fit(X, Y.mb(w), nb_[w], cq[q], last, len, lo + dur) - dur;
+        T.cand(q) = fit(X, Y.mb(w), T.nb(w), T.cq(q), last, len, lo + dur) - dur;
       }
     }
     for (;;) {
       int bq = -1;
       long long bt = kInf64;
       for (int q = 0; q < C; ++q)
-        if (cand[q] < bt) {
-          bt = cand[q];
+        if (T.cand(q) < bt) {
+          bt = T.cand(q);
           bq = q;
         }
       if (bq < 0) break;
       const long long e = bt + dur;
       X.at(Y.gf + (long long)bq * S + s) = e;
-      X.at(Y.ga + ((long long)bq * S + s - 1) * R + (mq[bq] & RM)) = e + wl2;
+      X.at(Y.ga + ((long long)bq * S + s - 1) * R + (T.mq(bq) & RM)) = e + wl2;
       last = e;
-      ++mq[bq];
-      cand[bq] = kInf64;
-      if (mq[bq] < M) {
-        const long long r = s == S - 1 ? X.at(Y.fdl + (long long)bq * R + (mq[bq] & RM))
-                                       : X.at(Y.ga + ((long long)bq * S + s) * R + (mq[bq] & RM));
-        cand[bq] = fit(X, Y.mb(w), nb_[w], cq[bq], last, len, imax(r, e) + dur) - dur;
+      ++T.mq(bq);
+      T.cand(bq) = kInf64;
+      if (T.mq(bq) < M) {
+        const long long r = s == S - 1 ? X.at(Y.fdl + (long long)bq * R + (T.mq(bq) & RM))
+                                       : X.at(Y.ga + ((long long)bq * S + s) * R + (T.mq(bq) & RM));
+        T.cand(bq) = fit(X, Y.mb(w), T.nb(w), T.cq(bq), last, len, imax(r, e) + dur) - dur;
       }
       for (int q = 0; q < C; ++q)  // candidates pushed by the new reservation
-        if (q != bq && cand[q] != kInf64 && cand[q] + dur < last + len)
-          cand[q] = fit(X, Y.mb(w), nb_[w], cq[q], last, len, cand[q] + dur) - dur;
+        if (q != bq && T.cand(q) != kInf64 && T.cand(q) + dur < last + len)
+          T.cand(q) = fit(X, Y.mb(w), T.nb(w), T.cq(q), last, len, T.cand(q) + dur) - dur;
     }
     for (int q = 0; q < C; ++q) mk = imax(mk, X.at(Y.gf + (long long)q * S + s));
   }
@@ -346,6 +373,9 @@ __global__ void __launch_bounds__(kEvalThreads, 4) atlas_seq_kernel(EvalArgs a) 
   const int lane = threadIdx.x & 31;
   const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   SeqMem X{a.scratch + gwarp * a.scratch_per_warp + (long long)lane * (a.scratch_per_warp / 32)};
+  extern __shared__ __align__(16) unsigned char seq_smem[];
+  SeqSmall T{(long long*)seq_smem, (int*)(seq_smem + 22 * 8 * kEvalThreads),
+             (signed char*)(seq_smem + (22 * 8 + 58 * 4) * kEvalThreads), (int)threadIdx.x};
   for (;;) {
     const int wk = atomicAdd(a.cursor, 1);
     if (wk >= a.n_work) break;
@@ -362,7 +392,7 @@ __global__ void __launch_bounds__(kEvalThreads, 4) atlas_seq_kernel(EvalArgs a) 
     r.scenario = si;
     r.d = d;
     if (g.feasible) {
-      const long long mk = atlas_seq_row<SMAX>(g, sc.mem_limit, X);
+      const long long mk = atlas_seq_row<SMAX>(g, sc.mem_limit, X, T);
       finish_row(sc, tp, g, mk, r);
       if (mk < 0) {
         r.feasible = -1;
@@ -382,26 +412,40 @@ long long atlas_seq_slice(int C, int S, int M, int nw, int L) {
          (long long)nw * (2LL * C * M + 2LL * M);
 }
 
+static void seq_smem_attrs() {
+  static bool done = false;  // per process; the attribute is per function
+  if (done) return;
+  cudaFuncSetAttribute(atlas_seq_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kSeqSmallBytes);
+  cudaFuncSetAttribute(atlas_seq_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kSeqSmallBytes);
+  cudaFuncSetAttribute(atlas_seq_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kSeqSmallBytes);
+  done = true;
+}
+
 int atlas_seq_blocks_per_sm(int smax) {
+  seq_smem_attrs();
   int n = 0;
   const cudaError_t e =
       smax <= 4 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_seq_kernel<4>,
-                                                                kEvalThreads, 0)
+                                                                kEvalThreads, kSeqSmallBytes)
       : smax <= 8 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_seq_kernel<8>,
-                                                                  kEvalThreads, 0)
+                                                                  kEvalThreads, kSeqSmallBytes)
                   : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_seq_kernel<16>,
-                                                                  kEvalThreads, 0);
+                                                                  kEvalThreads, kSeqSmallBytes);
   return e == cudaSuccess ? n : 1;
 }
 
 // smax: 4, 8 or 16 (rows with S <= smax)
 cudaError_t launch_atlas_seq(int smax, const EvalArgs& a, int grid, cudaStream_t st) {
+  seq_smem_attrs();
   if (smax <= 4)
-    atlas_seq_kernel<4><<<grid, kEvalThreads, 0, st>>>(a);
+    atlas_seq_kernel<4><<<grid, kEvalThreads, kSeqSmallBytes, st>>>(a);
   else if (smax <= 8)
-    atlas_seq_kernel<8><<<grid, kEvalThreads, 0, st>>>(a);
+    atlas_seq_kernel<8><<<grid, kEvalThreads, kSeqSmallBytes, st>>>(a);
   else
-    atlas_seq_kernel<16><<<grid, kEvalThreads, 0, st>>>(a);
+    atlas_seq_kernel<16><<<grid, kEvalThreads, kSeqSmallBytes, st>>>(a);
   return cudaGetLastError();
 }
 
