@@ -6,8 +6,9 @@ horizon = the largest makespan of the 1000), bubbletea.cpp:269-284) is
 packed FCFS into each plan's bubbles (schedule_prefills,
 bubbletea.cpp:132-222).
 
-* test_config4_golden: the 2*10^4-request prefix of that trace on six of the
-  plans (all four policies, D = 50 / 66 / 100 / 200: the deepest pruning
+* test_config4_golden: the 2*10^4-request prefix of that trace on twelve of
+  the plans (all four policies, D = 50 / 66 / 100 / 200, ranks 0 .. 999 of
+  the 1000: the deepest pruning
   paths — room-bound caps, the failure memo at minimum arrival, zero-layer
   stage runs for D > inference_layers), bit-exact against fixtures frozen
   from the reference's own schedule_prefills (oracle/_ref) by
