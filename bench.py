@@ -527,6 +527,12 @@ def impl_ours(args):
     clocks.start()
     for k in range(args.steps):
         l2_flush.fill_(k & 0xff)  # > L2 (126 MB): every step starts cold
+        if world > 1:
+            # align the ranks' step starts (outside the timed events): a rank
+            # that started early would otherwise count its wait for the
+            # slowest rank inside the winner all-gather as its own step time
+            torch.cuda.synchronize()
+            dist.barrier()
         starts[k].record(stream)
         planner.evaluate(sync=False)
         gather_best()
