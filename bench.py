@@ -484,7 +484,7 @@ def impl_ours(args):
     world, rank, local = dist_env()
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = local if world > 1 else 0
     torch.cuda.set_device(device)
     stream = torch.cuda.Stream()  # one non-default stream for every launch and event
