@@ -57,6 +57,7 @@ static_assert(sizeof(DevScen) == 112 || sizeof(DevScen) == 128, "DevScen size");
 // WAN boundary.
 struct Geom {
   int32_t feasible;
+  int32_t drain_lane;  // min S for the one-lane WAN drain greedy (C <= 4), 0 = never; set by the caller
   int32_t S, M, C, D;
   int32_t nb;
   int32_t blk_first[GPB_MAX_DC + 1];   // blk_first[nb] == S

@@ -38,6 +38,7 @@ __device__ __forceinline__ bool begin_row(const EvalArgs& a, int row, Geom& g,
   tp = &a.topos[sc->topo];
   const int d = (int)(row - sc->first_row) + 1;
   decode(*sc, *tp, d, g);
+  g.drain_lane = a.drain_lane;
   if (!g.feasible) {
     if ((threadIdx.x & 31) == 0) {
       gpb_row r;

@@ -718,7 +718,7 @@ static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
   for (size_t k = 0; k < n_side; ++k) cudaStreamWaitEvent(c.side[k], c.fork_ev, 0);
   const bool bt = c.bucket_timing;  // per-bucket events (profiling, roofline)
   if (bt) rec(c.bucket_ev[c.buckets.size()], st);
-  for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
+  for (size_t bi : c.launch_order) {  // longest estimate first
     const Bucket& b = c.buckets[bi];
     cudaStream_t ss = c.side[b.stream];
     if (bt) rec(c.bucket_ev[bi], ss);
@@ -738,6 +738,7 @@ static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
     a.error_flag = err_flag;
     a.row_cycles = c.profile_rows ? (long long*)c.b_cycles.ptr : nullptr;
     a.row_phase = a.row_cycles ? a.row_cycles + c.n_rows : nullptr;
+    a.drain_lane = c.drain_lane;
     const int grid = std::min(grid_eval, (b.count + 3) / 4);
     cudaError_t e;
     if (b.policy == GPB_GPIPE || b.policy == GPB_VARUNA) {
@@ -809,10 +810,18 @@ static int prepare_evaluate(Ctx& c) {
     return c.cuda_fail(cudaGetLastError(), "event");
   // buckets run concurrently on side streams forked from the launch stream
   c.n_side = std::max<size_t>(1, std::min<size_t>(kSideStreams, c.buckets.size()));
+  // Side stream 0 carries the longest-estimate bucket (LPT below) and runs at
+  // the highest priority, so the critical rows' CTAs are dispatched first
+  // when the buckets co-run; graph replays keep it (per-node priorities).
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  const char* penv = std::getenv("GPB_PRIO");
+  if (penv && penv[0] == '0') prio_hi = prio_lo;
   while (c.side.size() < c.n_side) {
     cudaStream_t s2;
     cudaEvent_t e2;
-    if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess ||
+    if (cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking,
+                                     c.side.empty() ? prio_hi : prio_lo) != cudaSuccess ||
         cudaEventCreateWithFlags(&e2, cudaEventDisableTiming) != cudaSuccess)
       return c.cuda_fail(cudaGetLastError(), "side streams");
     c.side.push_back(s2);
@@ -891,6 +900,7 @@ static int prepare_evaluate(Ctx& c) {
       load[si] += c.buckets[i].est;
       c.buckets[i].stream = (int)si;
     }
+    c.launch_order = ord;
   }
   c.eval_ready = true;
   return GPB_OK;
@@ -926,6 +936,8 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
   // device (0.563 vs 0.549 ms). GPB_GRAPH=0 launches directly.
   const char* genv = std::getenv("GPB_GRAPH");
   const bool use_graph = !(genv && genv[0] == '0');
+  const char* dl = std::getenv("GPB_DRAIN_LANE");
+  c.drain_lane = dl ? std::atoi(dl) : 32;
   if (!use_graph) {
     const int rc = record_evaluate(c, st, false);
     if (rc != GPB_OK) return rc;
@@ -936,6 +948,7 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     key.push_back(c.bucket_timing);
     key.push_back(c.profile_rows);
     key.push_back(c.sel_blocks);
+    key.push_back(c.drain_lane);
     for (const Bucket& b : c.buckets)
       for (long long v : {(long long)b.policy, (long long)b.B, (long long)b.offset,
                           (long long)b.count, (long long)b.gw, (long long)b.stream,
@@ -956,7 +969,8 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
         return rc;
       }
       if (ce != cudaSuccess) return c.cuda_fail(ce, "graph capture");
-      const cudaError_t ie = cudaGraphInstantiate(&c.graph_exec, g, 0);
+      const cudaError_t ie =
+          cudaGraphInstantiate(&c.graph_exec, g, cudaGraphInstantiateFlagUseNodePriority);
       cudaGraphDestroy(g);
       if (ie != cudaSuccess) {
         c.graph_exec = nullptr;

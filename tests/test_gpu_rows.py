@@ -195,6 +195,21 @@ def test_graph_mode_reloads(planner, checker, monkeypatch, graph):
     assert _compare_space(planner, checker, None, topos4, scens4) > 80
 
 
+@pytest.mark.parametrize("lane", ["1", "0"])
+def test_drain_greedy_variants(planner, checker, monkeypatch, lane):
+    """The WAN-stage drain greedy runs on one lane (C <= 4, S >= GPB_DRAIN_LANE,
+    default 32) or warp-wide; force each on every eligible row (the graph key
+    carries the switch, so the same load re-captures): rows stay bit-exact."""
+    monkeypatch.setenv("GPB_DRAIN_LANE", lane)
+    for ml, ms in ((1, 89.0), (2, 67.0), (6, 36.0), (0, 36.0)):
+        topos, sc = fixtures.unit12(policy="atlas", mem_limit=ml)
+        assert planner.select(topos, sc).rows[0].pp_time_ms == ms
+    topos, scens = random_space(2024, 120, wide=False)
+    assert _compare_space(planner, checker, None, topos, scens) > 120
+    topos, scens = random_space(77, 60, wide=True)
+    assert _compare_space(planner, checker, None, topos, scens) > 60
+
+
 def test_validator_accepts_every_policy(planner):
     """validate_timeline (validate.h:77-256) on the device: every feasible
     row's own timeline is valid (completeness, GPU and link exclusivity,
