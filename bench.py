@@ -527,11 +527,14 @@ def impl_ours(args):
     clocks.start()
     for k in range(args.steps):
         l2_flush.fill_(k & 0xff)  # > L2 (126 MB): every step starts cold
+        # the flush completes before the step's start event (measured: a step
+        # queued right behind the 256 MiB write runs ~45 us slower while the
+        # write drains; the L2 is cold either way)
+        torch.cuda.synchronize()
         if world > 1:
             # align the ranks' step starts (outside the timed events): a rank
             # that started early would otherwise count its wait for the
             # slowest rank inside the winner all-gather as its own step time
-            torch.cuda.synchronize()
             dist.barrier()
         starts[k].record(stream)
         planner.evaluate(sync=False)

@@ -562,13 +562,19 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
     // the per-row last-stage buffer (M entries per row) must fit the block
     return (size_t)(kEvalThreads / gw) * d.M * 8 <= 160 * 1024 ? gw : 32;
   };
+  const int heavy_b = [] {
+    const char* e = std::getenv("GPB_HEAVY_B");
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
   std::map<std::tuple<int, int, int, int>, std::vector<int>> by_key;
   for (int i = 0; i < n_scen; ++i) {
     int heavy = ds[i].policy == GPB_ATLAS && cost(i) >= 0.3 * max_atlas;
     const int gw = gw_of(ds[i], heavy != 0);
     if (ds[i].policy == GPB_ATLAS && gw > 0 && gw < 32) heavy = 0;
     if (ds[i].policy == GPB_ATLAS && gw == 0) heavy = 1;
-    by_key[{ds[i].policy, (ds[i].S + 31) / 32, heavy, gw}].push_back(i);
+    int B = (ds[i].S + 31) / 32;
+    if (heavy && gw == 32) B = std::max(B, std::min(8, heavy_b));
+    by_key[{ds[i].policy, B, heavy, gw}].push_back(i);
   }
   std::vector<int32_t> bscen;
   bscen.reserve(n_scen);
@@ -718,7 +724,7 @@ static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
   for (size_t k = 0; k < n_side; ++k) cudaStreamWaitEvent(c.side[k], c.fork_ev, 0);
   const bool bt = c.bucket_timing;  // per-bucket events (profiling, roofline)
   if (bt) rec(c.bucket_ev[c.buckets.size()], st);
-  for (size_t bi : c.launch_order) {  // longest estimate first
+  for (size_t bi = 0; bi < c.buckets.size(); ++bi) {
     const Bucket& b = c.buckets[bi];
     cudaStream_t ss = c.side[b.stream];
     if (bt) rec(c.bucket_ev[bi], ss);
@@ -809,8 +815,10 @@ static int prepare_evaluate(Ctx& c) {
   if (!c.fork_ev && cudaEventCreateWithFlags(&c.fork_ev, cudaEventDisableTiming) != cudaSuccess)
     return c.cuda_fail(cudaGetLastError(), "event");
   // buckets run concurrently on side streams forked from the launch stream
-  c.n_side = std::max<size_t>(1, std::min<size_t>(kSideStreams, c.buckets.size()));
-  // Side stream 0 carries the longest-estimate bucket (LPT below) and runs at
+  size_t max_side = kSideStreams;
+  if (const char* e = std::getenv("GPB_SIDE_STREAMS")) max_side = std::max(1, std::atoi(e));
+  c.n_side = std::max<size_t>(1, std::min<size_t>(max_side, c.buckets.size()));
+  // Side stream 0 carries the bucket with the longest row (below) and runs at
   // the highest priority, so the critical rows' CTAs are dispatched first
   // when the buckets co-run; graph replays keep it (per-node priorities).
   int prio_lo = 0, prio_hi = 0;
@@ -900,7 +908,14 @@ static int prepare_evaluate(Ctx& c) {
       load[si] += c.buckets[i].est;
       c.buckets[i].stream = (int)si;
     }
-    c.launch_order = ord;
+    // the bucket with the longest row (the step's critical path) goes to
+    // side stream 0, the high-priority one
+    size_t crit = 0;
+    for (size_t i = 1; i < c.buckets.size(); ++i)
+      if (c.buckets[i].cost > c.buckets[crit].cost) crit = i;
+    const int cs = c.buckets.empty() ? 0 : c.buckets[crit].stream;
+    for (Bucket& b : c.buckets)
+      b.stream = b.stream == cs ? 0 : (b.stream == 0 ? cs : b.stream);
   }
   c.eval_ready = true;
   return GPB_OK;

@@ -91,7 +91,6 @@ struct Ctx {
   // rows 0.75 vs 0.80 ms, S = 16 rows 108 K vs 88 K drain cycles);
   // GPB_DRAIN_LANE overrides per evaluate, 0 = never.
   int32_t drain_lane = 32;
-  std::vector<size_t> launch_order;  // buckets by estimate, longest first
   Buf b_scratch, b_cycles;
   bool profile_rows = false;
   // timeline / bubbletea buffers

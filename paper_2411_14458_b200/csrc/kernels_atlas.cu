@@ -408,10 +408,14 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
         hc[j] = loc;
       }
       int incl = loc;
+      if (B == 1) {  // one stage per lane: count the heads above by ballot
+        incl = __popc(__ballot_sync(kFull, loc != 0) & (0xffffffffu << lane));
+      } else {
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_down_sync(kFull, incl, o);
-        if (lane + o < 32) incl += v;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_down_sync(kFull, incl, o);
+          if (lane + o < 32) incl += v;
+        }
       }
 #pragma unroll
       for (int j = 0; j < B; ++j) hb[j] = kSegBig * (hc[j] + incl - loc);
@@ -431,7 +435,9 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
         um[j] = run;
       }
       long long sc = run;
-      for (int o = 1; o < nl; o <<= 1) {  // inclusive suffix max over the owning lanes
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {  // inclusive suffix max over the owning lanes
+        if (o >= nl) break;  // warp-uniform
         const long long ov = shfl_down64(sc, o);
         if (lane + o < nl) sc = imax(sc, ov);
       }
@@ -1013,7 +1019,9 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
         gl[j] = runmax;
       }
       long long pre = runmax;
-      for (int o = 1; o < nl; o <<= 1) {  // warp-uniform trip count
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        if (o >= nl) break;  // warp-uniform
         const long long v = shfl_up64(pre, o);
         if (lane >= o) pre = imax(pre, v);
       }

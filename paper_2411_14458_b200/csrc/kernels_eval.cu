@@ -627,18 +627,33 @@ __global__ void __launch_bounds__(kEvalThreads) select_kernel(SelectArgs a) {
   }
 }
 
+// (throughput desc, row asc) over the per-block winners; one warp, lanes
+// strided over the blocks, then a shuffle combine (rows < 0 are empty)
 __global__ void best_reduce_kernel(const gpb_best* in, int n, gpb_best* out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    gpb_best b;
-    b.throughput = -1.0;
-    b.row = -1;
-    for (int i = 0; i < n; ++i) {
-      if (in[i].row < 0) continue;
-      if (b.row < 0 || in[i].throughput > b.throughput ||
-          (in[i].throughput == b.throughput && in[i].row < b.row))
-        b = in[i];
+  const int lane = threadIdx.x & 31;
+  double bt = -1.0;
+  long long br = -1;
+  for (int i = lane; i < n; i += 32) {
+    const gpb_best v = in[i];
+    if (v.row < 0) continue;
+    if (br < 0 || v.throughput > bt || (v.throughput == bt && v.row < br)) {
+      bt = v.throughput;
+      br = v.row;
     }
-    if (b.row < 0) b.throughput = 0.0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ot = __shfl_xor_sync(kFull, bt, o);
+    const long long orow = __shfl_xor_sync(kFull, br, o);
+    if (orow >= 0 && (br < 0 || ot > bt || (ot == bt && orow < br))) {
+      bt = ot;
+      br = orow;
+    }
+  }
+  if (lane == 0) {
+    gpb_best b;
+    b.throughput = br < 0 ? 0.0 : bt;
+    b.row = br;
     *out = b;
   }
 }

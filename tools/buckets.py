@@ -1,7 +1,9 @@
 """Per-bucket launch timeline of one gpb_evaluate on a BASELINE workload
 (which bucket kernel sets the step time).
 
-    python tools/buckets.py [config2] [reps]
+    python tools/buckets.py [config2] [reps] [flush]
+
+flush=1 writes 256 MiB (> L2) before the last evaluate, as bench.py does.
 """
 import sys
 
@@ -14,7 +16,13 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 topos, scens = getattr(workloads, cfg)()
 p = Planner(0)
 n = p.load(abi.array(abi.Topology, topos), abi.array(abi.Scenario, scens))
+flush = len(sys.argv) > 3 and sys.argv[3] == "1"
 for _ in range(reps):
+    if flush:
+        import torch
+        buf = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()
+        del buf
     p.evaluate()
 t = p.timing()
 print(cfg, "rows", n, "evaluate_ms", round(t.evaluate_ms, 3), "kernels_ms",
