@@ -764,6 +764,7 @@ static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
       a.scratch_per_warp = P.scratch_per_warp;
       a.scratch_big_off = P.scratch_big_off;
       a.scratch = P.scratch_per_warp > 0 ? (long long*)c.b_scratch.ptr + c.scr_off[bi] : nullptr;
+      if (b.heavy && b.gw == 32 && c.heavy_excl) a.smem_floor = c.smem_optin;
       e = b.gw == 0   ? launch_atlas_wave(a, P.grid, P.wpc, ss)
           : b.gw < 32 ? launch_atlas_seq(b.gw, a, P.grid, ss)
                       : launch_atlas(b.B, a, P.grid, P.wpc, ss);
@@ -884,6 +885,15 @@ static int prepare_evaluate(Ctx& c) {
     const int rc = plan_atlas(c, b.B, false, b.max_c, b.max_s, b.max_m, b.max_nw, b.max_csm,
                               b.count, c.aplan[bi]);
     if (rc != GPB_OK) return rc;
+    if (!b.heavy) {
+      // small (latency-bound) spaces: the bulk ATLAS rows keep one CTA per
+      // SM so the flush/1F1B buckets launched beside them find room at once
+      // (config 2: 0.551 -> 0.521 ms; their last kernel ended at 0.53 ms
+      // behind two bulk CTAs per SM, now at 0.44 ms)
+      const char* e = std::getenv("GPB_BULK_PER_SM");
+      const int cap = e ? std::atoi(e) : (c.n_rows < group_flush_min_rows() ? 1 : 0);
+      if (cap > 0) c.aplan[bi].grid = std::max(1, std::min(c.aplan[bi].grid, c.num_sms * cap));
+    }
     if (std::getenv("GPB_DEBUG_PLAN"))
       std::fprintf(stderr, "atlas bucket %zu B=%d rows=%d C=%d S=%d M=%d nw=%d csm=%lld cap=%lld "
                    "total=%zu big_in_smem=%d wpc=%d grid=%d spw=%lld\n", bi, b.B, b.count,
@@ -953,6 +963,11 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
   const bool use_graph = !(genv && genv[0] == '0');
   const char* dl = std::getenv("GPB_DRAIN_LANE");
   c.drain_lane = dl ? std::atoi(dl) : 32;
+  // small (latency-bound) spaces: the heavy ATLAS CTAs get whole SMs
+  // (config 2: heavy bucket 0.511 -> 0.489 ms); saturated spaces keep the
+  // SMs shared (config 5 with it: 204 -> 237 ms)
+  const char* hx = std::getenv("GPB_HEAVY_EXCL");
+  c.heavy_excl = hx ? std::atoi(hx) : (c.n_rows < group_flush_min_rows() ? 1 : 0);
   if (!use_graph) {
     const int rc = record_evaluate(c, st, false);
     if (rc != GPB_OK) return rc;
@@ -964,6 +979,7 @@ int gpb_evaluate(gpb_ctx* ctx_, int32_t sync) {
     key.push_back(c.profile_rows);
     key.push_back(c.sel_blocks);
     key.push_back(c.drain_lane);
+    key.push_back(c.heavy_excl);
     for (const Bucket& b : c.buckets)
       for (long long v : {(long long)b.policy, (long long)b.B, (long long)b.offset,
                           (long long)b.count, (long long)b.gw, (long long)b.stream,

@@ -91,6 +91,10 @@ struct Ctx {
   // rows 0.75 vs 0.80 ms, S = 16 rows 108 K vs 88 K drain cycles);
   // GPB_DRAIN_LANE overrides per evaluate, 0 = never.
   int32_t drain_lane = 32;
+  // heavy ATLAS bucket's CTAs reserve a whole SM's shared memory (no other
+  // bucket's CTAs with shared memory co-reside with the critical rows);
+  // set per evaluate (GPB_HEAVY_EXCL, default on for small spaces)
+  int32_t heavy_excl = 0;
   Buf b_scratch, b_cycles;
   bool profile_rows = false;
   // timeline / bubbletea buffers

@@ -34,6 +34,7 @@ struct EvalArgs {
   const long long* tl_off;
   // flush: per-warp shared fd_last buffer length (max M of the bucket)
   int32_t smem_m;
+  int32_t smem_floor;         // atlas warp kernel: dynamic shared memory at least this (bytes)
   int32_t drain_lane;         // atlas: WAN-stage drain greedy on one lane when C <= 4 and S >= this (0 = never)
   // atlas: per-warp shared slice and (when it does not fit) global garr
   AtlasLayout lay;

@@ -1696,7 +1696,7 @@ cudaError_t launch_atlas_timeline(int B, const EvalArgs& a, int grid, int wpc, c
 
 template <int B>
 static cudaError_t launch_atlas_b(const EvalArgs& a, int grid, int wpc, cudaStream_t st) {
-  const size_t smem = (size_t)wpc * a.lay.total;
+  const size_t smem = std::max((size_t)wpc * a.lay.total, (size_t)a.smem_floor);
   cudaError_t e = ensure_smem_attr<B, false>(smem);
   if (e != cudaSuccess) return e;
   if (a.row_phase)
