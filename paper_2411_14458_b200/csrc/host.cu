@@ -521,10 +521,14 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   // ATLAS rows within 30% of the heaviest estimate form their own "heavy"
   // bucket, launched first (few warps, the critical path); the short
   // flush/1F1B buckets follow, then the bulk ATLAS rows fill the GPU.
+  static const double kFlushK = [] {
+    const char* e = std::getenv("GPB_FLUSH_COST");
+    return e ? std::atof(e) : 20.0;
+  }();
   auto cost = [&](int i) {
     const DevScen& d = ds[i];
     return d.policy == GPB_ATLAS ? (double)d.C * d.M * (2000.0 * d.C + 250.0 * d.S)
-                                 : 20.0 * d.M * d.S;
+                                 : kFlushK * (d.policy == GPB_1F1B ? 1.5 : 1.0) * d.M * d.S;
   };
   double max_atlas = 0;
   for (int i = 0; i < n_scen; ++i)

@@ -544,13 +544,20 @@ __device__ void drain_stage_scan(const Geom& g, AtlasMem& X, int s) {
     bool rs[K], act[K];
     int rs_first = K;
     long long acc = kNegMP;
+    // (p, m) of the lane's first pair, then stepped (no division per pair)
+    const int idx0 = base + lane * kk;
+    const int p0 = idx0 / M, mm0 = idx0 - p0 * M;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       u[i] = kNegMP;
       rs[i] = act[i] = false;
-      const int idx = base + lane * kk + i;
+      const int idx = idx0 + i;
       if (i < kk && idx < base + rem) {
-        const int p = idx / M, m = idx - p * M;
+        int p = p0, m = mm0 + i;
+        while (m >= M) {
+          m -= M;
+          ++p;
+        }
         const int m0 = X.nm[p * S + s];
         if (m >= m0) {
           act[i] = true;
@@ -596,8 +603,11 @@ __device__ void drain_stage_scan(const Geom& g, AtlasMem& X, int s) {
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       if (!act[i]) continue;
-      const int idx = base + lane * kk + i;
-      const int p = idx / M, m = idx - p * M;
+      int p = p0, m = mm0 + i;
+      while (m >= M) {
+        m -= M;
+        ++p;
+      }
       const long long uu = i >= rs_first ? u[i] : imax(pre, u[i]);
       const long long e = (long long)(m + 1) * dur + uu;
       if (s > 0) X.garr[((size_t)p * S + s - 1) * M + m] = e;
@@ -643,6 +653,7 @@ __device__ void drain_run_wavefront(const Geom& g, AtlasMem& X, int s_top, int s
   long long xo = 0;  // this lane's output of the previous step
   bool fo = false;   // ... and whether its bottom stage computed it
   long long top = 0;  // inputs of the run's top stage, items [t & ~31, +32), lane i = item +i
+  int wp = 0, wm = 0;
   for (int t = 0; t < n + nl - 1; ++t) {
     if ((t & 31) == 0 && t < n) {  // coalesced prefetch of the next 32 top inputs
       const int k = t + lane;
@@ -659,8 +670,12 @@ __device__ void drain_run_wavefront(const Geom& g, AtlasMem& X, int s_top, int s
       f = true;  // (a top stage always consumes the stored input)
     }
     const int k = t - lane;
+    if (k > 0 && ++wm == M) {  // (wp, wm) = pair k, stepped with t
+      wm = 0;
+      ++wp;
+    }
     if (lane < nl && k >= 0 && k < n) {
-      const int p = k / M, m = k - p * M;
+      const int p = wp, m = wm;
 #pragma unroll
       for (int j = 0; j < B; ++j) {
         const int s = sj[j];
@@ -764,11 +779,10 @@ __device__ void drain_stage_greedy(const Geom& g, AtlasMem& X, int s, int w) {
 template <bool TIMELINE, int CMAX>
 __device__ void drain_stage_greedy_lane(const Geom& g, AtlasMem& X, int s, int w) {
   {  // the stage's inputs (final: stage s+1 is drained), staged by the warp
-    const int S = g.S, M = g.M, n = g.C * g.M;
-    for (int i = threadIdx.x & 31; i < n; i += 32) {
-      const int q = i / M, m = i - q * M;
-      X.mtmp[i] = s == S - 1 ? X.fdl[q * M + m] : X.garr[((size_t)q * S + s) * M + m];
-    }
+    const int S = g.S, M = g.M, C = g.C;
+    for (int q = 0; q < C; ++q)
+      for (int m = threadIdx.x & 31; m < M; m += 32)
+        X.mtmp[q * M + m] = s == S - 1 ? X.fdl[q * M + m] : X.garr[((size_t)q * S + s) * M + m];
     __syncwarp();
   }
   if ((threadIdx.x & 31) == 0) {
