@@ -2,6 +2,9 @@
 
     python tests/golden/make_config4_golden.py TOP_PLANS.json [n_req=20000] [ranks...]
 
+(config4_pack_5e4.json: GOLDEN_OUT=... with n_req=50000 and ranks 52 2 1,
+then the duplicate top-1000 list dropped; it is the one in config4_pack.json.)
+
 Inputs: the config-3 top-1000 plan list by (throughput desc, row asc) as the
 GPU evaluated it (tools/dump_top_plans.py; its rows are pinned bit-exact to
 the reference by tests/test_gpu_scale.py / test_gpu_config2.py). For the
