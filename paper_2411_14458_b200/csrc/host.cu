@@ -543,9 +543,30 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   // bucket run one per thread (atlas_seq_kernel); GPB_ATLAS_SEQ=0 disables,
   // =2 also takes heavy rows (tests)
   const int seq_mode = atlas_seq_mode();
-  auto seq_ok = [&](const DevScen& d, bool heavy) {
+  // A row on one thread takes ~10-16x its warp-kernel time (measured: the
+  // slowest config-3 / config-5 thread rows, S = 14, C = 4, M = 64 / 256,
+  // 49 M / 126 M cycles against 3 M / 12 M estimated), and the seq buckets
+  // start their heaviest rows first, so in a plan-space shard the slowest
+  // thread rows set the step (config 5 at N = 8: the S <= 16 thread bucket
+  // ran 78.5 ms, every other bucket ended by 45 ms). Rows whose estimated
+  // cost exceeds the space's total cost / (8 warps x SMs x GPB_SEQ_RATIO)
+  // stay on a warp. Measured (tools/space_shard_rows.py, one GPU per shard):
+  // ratio 25 keeps configs 3 and 5 at N = 1 unchanged (26 / 205 ms) and
+  // takes config 3's N = 4 shard 19.2 -> 11.5 ms and config 5's N = 8 shard
+  // 75.7 -> 50.6 ms; larger ratios move more rows (config 5 N = 8: 32 ms at
+  // 300) but slow config 3 at N = 1 (26 -> 31 ms, its warp bucket
+  // saturates). 0 disables the cut.
+  static const double kSeqRatio = [] {
+    const char* e = std::getenv("GPB_SEQ_RATIO");
+    return e ? std::atof(e) : 25.0;
+  }();
+  double space_cost = 0;
+  for (int i = 0; i < n_scen; ++i) space_cost += cost(i) * ds[i].n_rows;
+  const double seq_cost_max =
+      kSeqRatio > 0 ? space_cost / (8.0 * std::max(1, c.num_sms) * kSeqRatio) : 1e300;
+  auto seq_ok = [&](const DevScen& d, bool heavy, double row_cost) {
     return seq_mode > 0 && n_rows >= group_min && d.S <= 16 && d.C <= 8 &&
-           (!heavy || seq_mode == 2) &&
+           (!heavy || seq_mode == 2) && (seq_mode == 2 || row_cost <= seq_cost_max) &&
            atlas_seq_slice(d.C, d.S, d.M, d.n_order - 1, d.mem_limit) <= kSeqMaxSlice;
   };
   const int wave_mode = atlas_wave_mode();
@@ -553,13 +574,13 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
     return wave_mode > 0 && (heavy || wave_mode == 2) && d.S <= 32 && d.C >= 2 &&
            d.C <= kWaveMaxPipes;
   };
-  auto gw_of = [&](const DevScen& d, bool heavy) {
+  auto gw_of = [&](const DevScen& d, bool heavy, double row_cost) {
     // ATLAS: 32 = one warp per row, 4 / 8 / 16 = one thread per row with
     // stage loops unrolled to that bound (atlas_seq_kernel<SMAX>), 0 = one
     // CTA per row with one warp per pipeline (atlas_wave_kernel)
     if (d.policy == GPB_ATLAS) {
       if (wave_ok(d, heavy)) return 0;
-      return seq_ok(d, heavy) ? (d.S <= 4 ? 4 : d.S <= 8 ? 8 : 16) : 32;
+      return seq_ok(d, heavy, row_cost) ? (d.S <= 4 ? 4 : d.S <= 8 ? 8 : 16) : 32;
     }
     if (kNoGroupFlush || n_rows < group_min) return 32;
     const int gw = d.S <= 8 ? 8 : (d.S <= 16 ? 16 : 32);
@@ -573,7 +594,7 @@ int gpb_load(gpb_ctx* ctx_, const gpb_topology* topos, int32_t n_topo,
   std::map<std::tuple<int, int, int, int>, std::vector<int>> by_key;
   for (int i = 0; i < n_scen; ++i) {
     int heavy = ds[i].policy == GPB_ATLAS && cost(i) >= 0.3 * max_atlas;
-    const int gw = gw_of(ds[i], heavy != 0);
+    const int gw = gw_of(ds[i], heavy != 0, cost(i));
     if (ds[i].policy == GPB_ATLAS && gw > 0 && gw < 32) heavy = 0;
     if (ds[i].policy == GPB_ATLAS && gw == 0) heavy = 1;
     int B = (ds[i].S + 31) / 32;
