@@ -536,6 +536,54 @@ __device__ void drain_stage_scan(const Geom& g, AtlasMem& X, int s) {
   const int S = g.S, M = g.M, C = g.C;
   const long long dur = g.dur;
   const int n = C * M;
+  // Few pairs left (the memory cap drained most of them in the forward
+  // phase, e.g. the config-2 critical row: ~8 of 256 per stage): one pass
+  // over the remaining pairs only, one per lane, instead of K pairs per lane
+  // over all C*M.
+  {
+    int rem_p = 0;
+    for (int p = lane; p < C; p += 32) rem_p += M - X.nm[p * S + s];
+    const int A = __reduce_add_sync(kFull, rem_p);
+    if (A <= 32) {
+      int p = 0, pre = 0, m0 = 0;
+      bool act = lane < A;
+      if (act) {  // the lane's pair: pipelines in order, pairs m0 .. M-1 of each
+        for (;; ++p) {
+          m0 = X.nm[p * S + s];
+          if (lane < pre + M - m0) break;
+          pre += M - m0;
+        }
+      }
+      const int m = m0 + lane - pre;
+      long long u = kNegMP;
+      bool f = true;
+      if (act) {
+        const long long r = s == S - 1 ? X.fdl[p * M + m] : X.garr[((size_t)p * S + s) * M + m];
+        u = r - (long long)m * dur;
+        f = m == m0;
+        if (f) u = imax(u, X.gf[p * S + s] - (long long)m0 * dur);
+      }
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {  // inclusive segmented max, upward
+        const long long ou = shfl_up64(u, o);
+        const bool of = __shfl_up_sync(kFull, (int)f, o) != 0;
+        if (lane >= o) {
+          if (!f) u = imax(u, ou);
+          f = f || of;
+        }
+      }
+      if (act) {
+        const long long e = (long long)(m + 1) * dur + u;
+        if (s > 0) X.garr[((size_t)p * S + s - 1) * M + m] = e;
+        if (TIMELINE) X.ps[((size_t)p * S + s) * M + m] = e - dur;
+        if (m == M - 1) X.gf[p * S + s] = e;
+      }
+      __syncwarp();
+      for (int q = lane; q < C; q += 32) X.nm[q * S + s] = M;
+      __syncwarp();
+      return;
+    }
+  }
   long long carry = kNegMP;
   for (int base = 0; base < n; base += 32 * K) {
     const int rem = n - base < 32 * K ? n - base : 32 * K;
@@ -705,6 +753,83 @@ __device__ void drain_run_wavefront(const Geom& g, AtlasMem& X, int s_top, int s
   __syncwarp();
   for (int i = lane; i < C * R; i += 32) X.nm[(i / R) * S + s_bot + i % R] = M;
   __syncwarp();
+}
+
+// A run s_bot..s_top of stages without a WAN gradient link in which every
+// pipeline p entered the drain with the same drained count n0 at every
+// stage of the run (e.g. no forced drains: mem_limit >= M, the deep config-2
+// rows), evaluation rows only. The run is a rectangular max-plus grid with
+// uniform cell weight dur: e[s][m] = max(e[s+1][m], e[s][m-1]) + dur,
+// e[s_top+1][m] = in[m] (the stored input of the top stage), e[s][n0-1] =
+// gf[s]. Every monotone path from an entry point to cell (s, m) has the same
+// number of cells, so
+//   e[s][m] = (m+1-s)*dur + max( max_{s <= s' <= s_top} gf[s'] + (s'-n0)*dur,
+//                                max_{n0 <= j <= m} in[j] + (s_top-j)*dur ),
+// exact in int64. Only what later stages and the row read is produced: the
+// bottom stage's outputs (the gradients of stage s_bot-1) and each stage's
+// last end (gpu_free, the makespan). O(C*(M + R)) instead of O(C*M*R).
+// Returns false (nothing done) when some pipeline's counts differ across
+// the run.
+__device__ bool drain_run_closed(const Geom& g, AtlasMem& X, int s_top, int s_bot) {
+  const int lane = threadIdx.x & 31;
+  const int S = g.S, M = g.M, C = g.C;
+  const long long dur = g.dur;
+  const int R = s_top - s_bot + 1;
+  bool bad = false;
+  for (int i = lane; i < C * R; i += 32) {
+    const int p = i / R, s = s_bot + i % R;
+    bad |= X.nm[p * S + s] != X.nm[p * S + s_top];
+  }
+  if (__any_sync(kFull, bad)) return false;
+  for (int p = 0; p < C; ++p) {
+    const int n0 = X.nm[p * S + s_top];
+    if (n0 >= M) continue;
+    // the gpu_free term over the whole run (its value at the bottom stage)
+    long long gs_all = kNegMP;
+    for (int s = s_bot + lane; s <= s_top; s += 32)
+      gs_all = imax(gs_all, X.gf[p * S + s] + (long long)(s - n0) * dur);
+    gs_all = warp_max64(gs_all);
+    // prefix max over the pairs of in[j] + (s_top - j) * dur: bottom outputs
+    long long pm = kNegMP;
+    for (int m0 = n0; m0 < M; m0 += 32) {
+      const int m = m0 + lane;
+      long long v = kNegMP;
+      if (m < M) {
+        const long long in = s_top == S - 1 ? X.fdl[p * M + m]
+                                            : X.garr[((size_t)p * S + s_top) * M + m];
+        v = in + (long long)(s_top - m) * dur;
+      }
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long ov = shfl_up64(v, o);
+        if (lane >= o) v = imax(v, ov);
+      }
+      v = imax(v, pm);
+      if (m < M && s_bot > 0)
+        X.garr[((size_t)p * S + s_bot - 1) * M + m] =
+            (long long)(m + 1 - s_bot) * dur + imax(gs_all, v);
+      pm = shfl_idx64(v, 31);
+    }
+    // every stage's last end: suffix max of the gpu_free term, 32 stages at a
+    // time from the top (each lane reads its stage before writing it)
+    long long gs = kNegMP;
+    for (int top = s_top; top >= s_bot; top -= 32) {
+      const int s = top - lane;
+      long long v = s >= s_bot ? X.gf[p * S + s] + (long long)(s - n0) * dur : kNegMP;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {  // max over lanes <= lane: stages >= s
+        const long long ov = shfl_up64(v, o);
+        if (lane >= o) v = imax(v, ov);
+      }
+      v = imax(v, gs);
+      if (s >= s_bot) X.gf[p * S + s] = (long long)(M - s) * dur + imax(v, pm);
+      gs = shfl_idx64(v, 31);
+    }
+    __syncwarp();
+  }
+  for (int i = lane; i < C * R; i += 32) X.nm[(i / R) * S + s_bot + i % R] = M;
+  __syncwarp();
+  return true;
 }
 
 // Stage s whose gradient link w crosses the WAN: per-stage greedy, lane q =
@@ -1136,6 +1261,11 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     // per-stage scans cost ~R * ceil(CM / 256) scan steps, the wavefront
     // CM + R/B shuffle steps (kWaveRatio: measured cost ratio of the two)
     const int R = s - sb + 1, CM = C * g.M;
+    if (!TIMELINE && drain_run_closed(g, X, s, sb)) {
+      s = sb - 1;
+      if (PROF) dph[2] += clock64() - td;
+      continue;
+    }
     if ((long long)(CM + (R + B - 1) / B) > (long long)kWaveRatio * R * ((CM + 255) / 256)) {
       for (; s >= sb; --s) drain_stage_scan<TIMELINE>(g, X, s);
       if (PROF) dph[1] += clock64() - td;
@@ -1452,6 +1582,10 @@ __device__ long long atlas_drain_all(const Geom& g, AtlasMem& X, const WaveState
     int sb = s;
     while (sb > 0 && X.wbs[sb - 1] < 0) --sb;
     const int R = s - sb + 1, CM = C * g.M;
+    if (!TIMELINE && drain_run_closed(g, X, s, sb)) {
+      s = sb - 1;
+      continue;
+    }
     if ((long long)(CM + (R + B - 1) / B) > (long long)kWaveRatio * R * ((CM + 255) / 256)) {
       for (; s >= sb; --s) drain_stage_scan<TIMELINE>(g, X, s);
       continue;
