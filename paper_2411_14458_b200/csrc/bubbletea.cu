@@ -715,7 +715,65 @@ __global__ void __launch_bounds__(32 * W, 1) pack_kernel(PackArgs a) {
     int pipe1 = -1;
     long long t1 = kInf64;
     unsigned long long failm = 0;  // pipelines < 64 that failed this lane's search
-    {
+    // Few active requests in the warp (the room bounds reject most of a long
+    // trace) on a plan with many stages: search them one after another with
+    // the whole warp (gs lanes per pipeline, ng pipelines at a time, the
+    // lowest success wins, failures below it recorded) instead of one lane
+    // per request walking all D stages alone. Same pipelines searched in the
+    // same order on the same batch-start state: identical answers.
+    bool has_cand = false;  // some pipeline's caps and memo admit it
+    if (act)
+      for (int pl = 0; pl < n_pipes && !has_cand; ++pl)
+        has_cand = rg.d0 <= capB[pl] && (extra == 0 || rg.d1 <= capA[pl]) &&
+                   !((memo[(size_t)pl * a.memo_words + (tok_l >> 5)] >> (tok_l & 31)) & 1u);
+    const unsigned actm = __ballot_sync(kFull, has_cand);
+    if (actm && gs >= 4 && __popc(actm) * 2 <= gs) {
+      const long long tc = clock64();
+      for (unsigned rem = actm; rem; rem &= rem - 1) {
+        const int src = __ffs(rem) - 1;
+        const long long arr_s = shfl_idx64(arrival, src);
+        ReqGeom rg_s;
+        rg_s.d0 = shfl_idx64(rg.d0, src);
+        rg_s.d1 = shfl_idx64(rg.d1, src);
+        rg_s.ovh = shfl_idx64(rg.ovh, src);
+        rg_s.extra = extra;
+        const int tok_s = __shfl_sync(kFull, tok_l, src);
+        int win = -1;
+        long long win_t = kInf64;
+        unsigned long long fm = 0;  // this lane's failed pipelines (< 64) below the winner
+        for (int c0 = 0; c0 < n_pipes && win < 0; c0 += 32) {
+          const int pl = c0 + lane;
+          bool cand = pl < n_pipes && rg_s.d0 <= capB[pl] && (extra == 0 || rg_s.d1 <= capA[pl]);
+          if (cand)
+            cand = !((memo[(size_t)pl * a.memo_words + (tok_s >> 5)] >> (tok_s & 31)) & 1u);
+          unsigned pmask = __ballot_sync(kFull, cand);
+          while (pmask && win < 0) {
+            const unsigned bit = __fns(pmask, 0, grp + 1);  // one survivor per group
+            const int pi = bit < 32 ? c0 + (int)bit : -1;
+            st_search += pi >= 0 && gl == 0;
+            const long long t = group_search<4>(a, sl, gb, pi, arr_s, rg_s, gs, st_iter, zrun);
+            const unsigned ok = __ballot_sync(kFull, gl == 0 && pi >= 0 && t != kInf64);
+            if (ok) {
+              const int wl = __ffs(ok) - 1;  // lowest group = lowest pipeline
+              win = __shfl_sync(kFull, pi, wl);
+              win_t = shfl_idx64(t, wl);
+            }
+            if (gl == 0 && pi >= 0 && pi < 64 && t == kInf64 && (win < 0 || pi < win)) {
+              fm |= 1ull << pi;
+              ++st_fail;
+            }
+            for (int g = 0; g < ng && pmask; ++g) pmask &= pmask - 1;
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) fm |= __shfl_xor_sync(kFull, fm, o);
+        if (lane == src) {
+          pipe1 = win;
+          t1 = win_t;
+          failm = fm;
+        }
+      }
+      st_cyc_search += clock64() - tc;
+    } else {
       const long long tc = clock64();
       for (;;) {
         int cand = -1;
