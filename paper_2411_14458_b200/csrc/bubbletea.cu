@@ -721,13 +721,22 @@ __global__ void __launch_bounds__(32 * W, 1) pack_kernel(PackArgs a) {
     // lowest success wins, failures below it recorded) instead of one lane
     // per request walking all D stages alone. Same pipelines searched in the
     // same order on the same batch-start state: identical answers.
-    bool has_cand = false;  // some pipeline's caps and memo admit it
+    // Cost model (stage checks per leapfrog round): one lane per request
+    // walks its candidates one by one, max over lanes of (candidates x
+    // d_eff); the warp takes the requests one by one, ng_c candidates at a
+    // time with groups of gs_c lanes: sum over requests of ceil(candidates /
+    // ng_c) x ceil(d_eff / gs_c).
+    int n_cand = 0;  // pipelines whose caps and memo admit the request
     if (act)
-      for (int pl = 0; pl < n_pipes && !has_cand; ++pl)
-        has_cand = rg.d0 <= capB[pl] && (extra == 0 || rg.d1 <= capA[pl]) &&
-                   !((memo[(size_t)pl * a.memo_words + (tok_l >> 5)] >> (tok_l & 31)) & 1u);
-    const unsigned actm = __ballot_sync(kFull, has_cand);
-    if (actm && gs >= 4 && __popc(actm) * 2 <= gs) {
+      for (int pl = 0; pl < n_pipes; ++pl)
+        n_cand += rg.d0 <= capB[pl] && (extra == 0 || rg.d1 <= capA[pl]) &&
+                  !((memo[(size_t)pl * a.memo_words + (tok_l >> 5)] >> (tok_l & 31)) & 1u);
+    const unsigned actm = __ballot_sync(kFull, n_cand > 0);
+    const int gs_c = gs < 4 ? gs : 4, ng_c = 32 / gs_c, grp_c = lane / gs_c, gl_c = lane & (gs_c - 1);
+    const int lane_cost = n_cand * d_eff;
+    const int coop_cost = ((n_cand + ng_c - 1) / ng_c) * ((d_eff + gs_c - 1) / gs_c);
+    if (actm && gs >= 4 &&
+        __reduce_add_sync(kFull, coop_cost) < __reduce_max_sync(kFull, lane_cost)) {
       const long long tc = clock64();
       for (unsigned rem = actm; rem; rem &= rem - 1) {
         const int src = __ffs(rem) - 1;
@@ -748,21 +757,21 @@ __global__ void __launch_bounds__(32 * W, 1) pack_kernel(PackArgs a) {
             cand = !((memo[(size_t)pl * a.memo_words + (tok_s >> 5)] >> (tok_s & 31)) & 1u);
           unsigned pmask = __ballot_sync(kFull, cand);
           while (pmask && win < 0) {
-            const unsigned bit = __fns(pmask, 0, grp + 1);  // one survivor per group
+            const unsigned bit = __fns(pmask, 0, grp_c + 1);  // one survivor per group
             const int pi = bit < 32 ? c0 + (int)bit : -1;
-            st_search += pi >= 0 && gl == 0;
-            const long long t = group_search<4>(a, sl, gb, pi, arr_s, rg_s, gs, st_iter, zrun);
-            const unsigned ok = __ballot_sync(kFull, gl == 0 && pi >= 0 && t != kInf64);
+            st_search += pi >= 0 && gl_c == 0;
+            const long long t = group_search<8>(a, sl, gb, pi, arr_s, rg_s, gs_c, st_iter, zrun);
+            const unsigned ok = __ballot_sync(kFull, gl_c == 0 && pi >= 0 && t != kInf64);
             if (ok) {
               const int wl = __ffs(ok) - 1;  // lowest group = lowest pipeline
               win = __shfl_sync(kFull, pi, wl);
               win_t = shfl_idx64(t, wl);
             }
-            if (gl == 0 && pi >= 0 && pi < 64 && t == kInf64 && (win < 0 || pi < win)) {
+            if (gl_c == 0 && pi >= 0 && pi < 64 && t == kInf64 && (win < 0 || pi < win)) {
               fm |= 1ull << pi;
               ++st_fail;
             }
-            for (int g = 0; g < ng && pmask; ++g) pmask &= pmask - 1;
+            for (int g = 0; g < ng_c && pmask; ++g) pmask &= pmask - 1;
           }
         }
         for (int o = 16; o > 0; o >>= 1) fm |= __shfl_xor_sync(kFull, fm, o);
