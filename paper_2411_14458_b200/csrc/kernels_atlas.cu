@@ -181,7 +181,34 @@ __device__ __forceinline__ void link_advance(const long long* mg, int n, LinkCur
                                              long long x) {
   if (c.v + len > x) return;
   const int cur = c.i;
-  int lo = cur + 1, step = 1;
+  // the next four entries in one round of independent loads (a query usually
+  // moves the cursor by about the number of earlier pipelines); past the end
+  // reads as kEndCur, which ends after every query
+  const long long v1 = cur + 1 < n ? mg[cur + 1] : kEndCur,
+                  v2 = cur + 2 < n ? mg[cur + 2] : kEndCur,
+                  v3 = cur + 3 < n ? mg[cur + 3] : kEndCur,
+                  v4 = cur + 4 < n ? mg[cur + 4] : kEndCur;
+  if (v1 + len > x) {
+    c.i = cur + 1;
+    c.v = v1;
+    return;
+  }
+  if (v2 + len > x) {
+    c.i = cur + 2;
+    c.v = v2;
+    return;
+  }
+  if (v3 + len > x) {
+    c.i = cur + 3;
+    c.v = v3;
+    return;
+  }
+  if (v4 + len > x) {
+    c.i = cur + 4;
+    c.v = v4;
+    return;
+  }
+  int lo = cur + 5, step = 1;
   while (lo + step - 1 < n && mg[lo + step - 1] + len <= x) {
     lo += step;
     step <<= 1;
