@@ -948,6 +948,54 @@ __device__ void drain_stage_greedy_lane(const Geom& g, AtlasMem& X, int s, int w
     long long gfq[CMAX], cand[CMAX];
     LinkCur cur[CMAX];
     long long last_a = kNegMP;
+    if (nmg == 0) {
+      // No forced drains on this link (mem_limit >= M): it holds only this
+      // stage's commits, in non-decreasing time, so earliest_fit of a
+      // transfer at x is max(x, last + len) and every candidate's start is
+      // max(raw_q, last + len - dur) with raw_q = max(input, gpu_free): the
+      // greedy is an argmin of that over the pipelines' next pairs (lowest
+      // pipeline on ties), no list walks.
+      long long raw[CMAX];
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q) {
+        mq[q] = q < C ? X.nm[q * S + s] : M;
+        gfq[q] = q < C ? X.gf[q * S + s] : 0;
+        raw[q] = mq[q] < M ? imax(in[q * M + mq[q]], gfq[q]) : kInf64;
+      }
+      long long floor_t = kNegMP;  // last + len - dur (len > 0)
+      for (;;) {
+        long long b = kInf64;
+        int bq = -1;
+#pragma unroll
+        for (int q = 0; q < CMAX; ++q) {
+          const long long st = imax(raw[q], floor_t);
+          if (raw[q] != kInf64 && st < b) {
+            b = st;
+            bq = q;
+          }
+        }
+        if (bq < 0) break;
+        const long long e = b + dur;
+        if (len > 0) floor_t = e + len - dur;
+#pragma unroll
+        for (int q = 0; q < CMAX; ++q) {
+          if (q == bq) {  // atlas_commit_pair (:298-317) + reserve
+            X.resb[((size_t)w * C + q) * M + mq[q]] = e;
+            X.garr[((size_t)q * S + s - 1) * M + mq[q]] = e + wl;
+            if (TIMELINE) X.ps[((size_t)q * S + s) * M + mq[q]] = b;
+            gfq[q] = e;
+            ++mq[q];
+            raw[q] = mq[q] < M ? imax(in[q * M + mq[q]], e) : kInf64;
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q)
+        if (q < C) {
+          X.gf[q * S + s] = gfq[q];
+          X.nm[q * S + s] = M;
+        }
+    } else {
 #pragma unroll
     for (int q = 0; q < CMAX; ++q) {
       cand[q] = kInf64;
@@ -1006,6 +1054,7 @@ __device__ void drain_stage_greedy_lane(const Geom& g, AtlasMem& X, int s, int w
         X.gf[q * S + s] = gfq[q];
         X.nm[q * S + s] = M;
       }
+    }
   }
   __syncwarp();
 }
