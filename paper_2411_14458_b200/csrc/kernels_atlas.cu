@@ -136,32 +136,44 @@ struct AtlasMem {
 // overlap: a monotone cursor over the static list plus one comparison with
 // the own tail answer free_at / earliest_fit (base.h:65-84) exactly.
 
-// first index >= i0 with v[i] >= x (v sorted), by bisection
-__device__ __forceinline__ int lower_idx(const long long* v, int n, long long x, bool upper) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (upper ? v[mid] <= x : v[mid] < x) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
+// past-the-end value of a list (above every time; see LinkCur)
+constexpr long long kEndCur = 1LL << 60;
 
-// A[0..na) <- merge(A, Bv[0..nb)) through tmp (warp-parallel merge path:
-// every element lands at its index plus its rank in the other list; A wins
-// ties).
+// A[0..na) <- merge(A, Bv[0..nb)) through tmp (warp-parallel; A wins ties).
 __device__ __forceinline__ void warp_merge(long long* A, int na, const long long* Bv, int nb,
                                            long long* tmp) {
+  // Merge path: lane l writes outputs [l*k, l*k + k); one bisection finds how
+  // many of A precede its first output (A[i] goes before Bv[j] iff A[i] <=
+  // Bv[j]), then a sequential two-cursor merge of its k outputs (one new
+  // load per output instead of a bisection per element).
   const int lane = threadIdx.x & 31;
-  for (int i = lane; i < na; i += 32) tmp[i + lower_idx(Bv, nb, A[i], false)] = A[i];
-  for (int j = lane; j < nb; j += 32) tmp[j + lower_idx(A, na, Bv[j], true)] = Bv[j];
+  const int n = na + nb, k = (n + 31) >> 5;
+  const int d = min(lane * k, n), d_end = min(d + k, n);
+  int lo = max(0, d - nb), hi = min(d, na);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (A[mid] <= Bv[d - mid - 1]) lo = mid + 1; else hi = mid;
+  }
+  int i = lo, j = d - lo;
+  long long a = i < na ? A[i] : kEndCur, b = j < nb ? Bv[j] : kEndCur;
+  for (int o = d; o < d_end; ++o) {
+    if (j >= nb || (i < na && a <= b)) {
+      tmp[o] = a;
+      ++i;
+      a = i < na ? A[i] : kEndCur;
+    } else {
+      tmp[o] = b;
+      ++j;
+      b = j < nb ? Bv[j] : kEndCur;
+    }
+  }
   __syncwarp();
-  for (int i = lane; i < na + nb; i += 32) A[i] = tmp[i];
+  for (int x = lane; x < n; x += 32) A[x] = tmp[x];
   __syncwarp();
 }
 
 // Cursor into a static list: index i and the entry there (kEndCur past the
 // end), so the common "no advance" check needs no load.
-constexpr long long kEndCur = 1LL << 60;
 struct LinkCur {
   int i;
   long long v;
