@@ -501,6 +501,7 @@ def impl_ours(args):
     l2_flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     best_t = torch.zeros(2, dtype=torch.int64, device="cuda")   # raw gpb_best
     gathered = torch.zeros(2 * world, dtype=torch.int64, device="cuda")
+    align_t = torch.zeros(1, dtype=torch.int32, device="cuda")
 
     def gather_best():
         if world > 1:
@@ -534,8 +535,13 @@ def impl_ours(args):
         if world > 1:
             # align the ranks' step starts (outside the timed events): a rank
             # that started early would otherwise count its wait for the
-            # slowest rank inside the winner all-gather as its own step time
+            # slowest rank inside the winner all-gather as its own step time.
+            # The host barrier brings the launches close; a one-word NCCL
+            # all-reduce on the stream then aligns the devices themselves
+            # (its completion, which the start event follows, is the same
+            # instant on every GPU up to the collective's own skew)
             dist.barrier()
+            dist.all_reduce(align_t)
         starts[k].record(stream)
         planner.evaluate(sync=False)
         gather_best()
