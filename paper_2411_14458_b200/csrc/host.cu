@@ -440,6 +440,14 @@ static int atlas_seq_mode() {
   const char* e = std::getenv("GPB_ATLAS_SEQ");
   return e ? std::atoi(e) : 1;
 }
+// The 4-blocks-per-SM ATLAS instantiation (kernels_atlas.cu OCC4) for spaces
+// large enough to be throughput-bound: measured config 5 (10^7 rows) 207 ->
+// 193 ms, but its N=8 shard (1.25*10^6 rows, bound by its slowest warp rows)
+// 50.6 -> 60.8 ms and small spaces' critical rows ~15 % slower.
+static int64_t occ4_min_rows() {
+  const char* e = std::getenv("GPB_OCC4_MIN_ROWS");
+  return e ? std::atoll(e) : 2000000;
+}
 static int64_t group_flush_min_rows() {
   const char* e = std::getenv("GPB_GROUP_FLUSH_MIN_ROWS");
   return e ? std::atoll(e) : 200000;
@@ -770,6 +778,7 @@ static int record_evaluate(Ctx& c, cudaStream_t st, bool cap) {
     a.row_cycles = c.profile_rows ? (long long*)c.b_cycles.ptr : nullptr;
     a.row_phase = a.row_cycles ? a.row_cycles + c.n_rows : nullptr;
     a.drain_lane = c.drain_lane;
+    a.occ4 = b.B == 1 && c.n_rows >= occ4_min_rows();
     const int grid = std::min(grid_eval, (b.count + 3) / 4);
     cudaError_t e;
     if (b.policy == GPB_GPIPE || b.policy == GPB_VARUNA) {
@@ -1297,7 +1306,8 @@ int plan_atlas(Ctx& c, int B, bool timeline, int C, int S, int M, int nw, long l
     return GPB_CONFIG_ERROR;
   }
   const size_t smem = (size_t)P.wpc * L.total;
-  int per_sm = atlas_blocks_per_sm(B, timeline, P.wpc, smem);
+  int per_sm = atlas_blocks_per_sm(B, timeline, P.wpc, smem,
+                                   B == 1 && !timeline && c.n_rows >= occ4_min_rows());
   per_sm = std::max(1, std::min(per_sm, (int)(sm_budget / smem)));
   P.grid = (int)std::max(1LL, std::min<long long>((long long)c.num_sms * per_sm,
                                                   (count + P.wpc - 1) / P.wpc));

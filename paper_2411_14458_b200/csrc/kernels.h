@@ -36,6 +36,7 @@ struct EvalArgs {
   int32_t smem_m;
   int32_t smem_floor;         // atlas warp kernel: dynamic shared memory at least this (bytes)
   int32_t drain_lane;         // atlas: WAN-stage drain greedy on one lane when C <= 4 and S >= this (0 = never)
+  int32_t occ4;               // atlas B = 1: the 4-blocks-per-SM instantiation (large spaces)
   // atlas: per-warp shared slice and (when it does not fit) global garr
   AtlasLayout lay;
   long long* scratch;
@@ -59,7 +60,7 @@ cudaError_t launch_flush_group(int gw, bool gpipe, const EvalArgs& a, int grid, 
 cudaError_t launch_onef1b(int B, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_onef1b_group(int gw, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_atlas(int B, const EvalArgs& a, int grid, int wpc, cudaStream_t st);
-int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem);
+int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem, bool occ4 = false);
 // one thread per ATLAS row (bulk of large spaces); scratch_per_warp = 32 x
 // the per-thread slice (int64 elements) for rows up to (C, S, M, nw)
 long long atlas_seq_slice(int C, int S, int M, int nw, int L);

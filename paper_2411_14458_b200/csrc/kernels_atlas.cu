@@ -1829,8 +1829,12 @@ cudaError_t launch_atlas_wave(const EvalArgs& a, int grid, int warps, cudaStream
 #define GPB_ATLAS_MIN_BLOCKS_B1 3
 #endif
 
-template <int B, bool PROF>
-__global__ void __launch_bounds__(kEvalThreads, B == 1 ? GPB_ATLAS_MIN_BLOCKS_B1 : 1)
+// OCC4 (one stage per lane, large spaces): 4 resident blocks per SM (128
+// registers, no spills): more rows in flight where throughput sets the step
+// (config 5: 207 -> 193 ms), while the latency-bound small spaces keep 3
+// (their critical rows ran ~15 % slower at 4: 805 K -> 935 K cycles).
+template <int B, bool PROF, bool OCC4 = false>
+__global__ void __launch_bounds__(kEvalThreads, B == 1 ? (OCC4 ? 4 : GPB_ATLAS_MIN_BLOCKS_B1) : 1)
     atlas_kernel(EvalArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
@@ -1903,6 +1907,14 @@ static cudaError_t ensure_smem_attr(size_t smem) {
   if (e == cudaSuccess && !TL)  // the profiling instantiation (gpb_set_profile)
     e = cudaFuncSetAttribute(atlas_kernel<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
+  if constexpr (B == 1) {  // the 4-blocks-per-SM instantiations
+    if (e == cudaSuccess && !TL)
+      e = cudaFuncSetAttribute(atlas_kernel<1, false, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess && !TL)
+      e = cudaFuncSetAttribute(atlas_kernel<1, true, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
   if (e == cudaSuccess && dev < 64) done[dev] = (int)smem;
   return e;
 }
@@ -1935,6 +1947,15 @@ static cudaError_t launch_atlas_b(const EvalArgs& a, int grid, int wpc, cudaStre
   const size_t smem = std::max((size_t)wpc * a.lay.total, (size_t)a.smem_floor);
   cudaError_t e = ensure_smem_attr<B, false>(smem);
   if (e != cudaSuccess) return e;
+  if constexpr (B == 1) {
+    if (a.occ4) {
+      if (a.row_phase)
+        atlas_kernel<1, true, true><<<grid, 32 * wpc, smem, st>>>(a);
+      else
+        atlas_kernel<1, false, true><<<grid, 32 * wpc, smem, st>>>(a);
+      return cudaGetLastError();
+    }
+  }
   if (a.row_phase)
     atlas_kernel<B, true><<<grid, 32 * wpc, smem, st>>>(a);
   else
@@ -1943,9 +1964,16 @@ static cudaError_t launch_atlas_b(const EvalArgs& a, int grid, int wpc, cudaStre
 }
 
 // Resident blocks per SM of the ATLAS kernel (registers + shared memory).
-int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem) {
+int atlas_blocks_per_sm(int B, bool timeline, int wpc, size_t smem, bool occ4) {
   int n = 0;
   cudaError_t e = cudaSuccess;
+  if (B == 1 && !timeline && occ4) {
+    e = ensure_smem_attr<1, false>(smem);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, atlas_kernel<1, false, true>, 32 * wpc,
+                                                        smem);
+    return e == cudaSuccess ? n : 0;
+  }
 #define GPB_OCC(BB)                                                                         \
   case BB:                                                                                  \
     e = timeline ? ensure_smem_attr<BB, true>(smem) : ensure_smem_attr<BB, false>(smem);      \
