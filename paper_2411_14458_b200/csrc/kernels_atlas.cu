@@ -372,26 +372,25 @@ __device__ __forceinline__ void atlas_cascade(const Geom& g, int p, int m, int L
   const int S = g.S, M = g.M, C = g.C;
   const int nl = (S + B - 1) / B;  // lanes owning stages
   const long long dur = g.dur;
-  // lowest blocked stage
-  int my_min = 0x7fffffff;
-#pragma unroll
-  for (int j = B - 1; j >= 0; --j)
-    if (lane * B + j < S && m - drr[j] >= L) my_min = lane * B + j;
-  const int s_min = __reduce_min_sync(kFull, my_min);
+  // Lowest blocked stage: a pair drains at stage s only after it drained at
+  // s+1 (its gradient), so drained[s] <= drained[s+1] and the callers (stage
+  // 0 blocked) always have s_min = 0: stage 0 drains to m - L + 1, every
+  // stage above it all its ready pairs, and the most pairs of any stage above
+  // are stage 1's (the fewest drained).
+  constexpr int s_min = 0;
   // pair counts, links (dm of the stage above: next local stage, or lane+1)
   int cnt[B];
   bool link[B];
   const int up_dm = __shfl_down_sync(kFull, drr[0], 1);
-  int nmax = 0;
 #pragma unroll
   for (int j = 0; j < B; ++j) {
     const int s = lane * B + j;
     cnt[j] = s >= S || s < s_min ? 0 : (s == s_min ? m - L + 1 - drr[j] : m - drr[j]);
     const int dma = j + 1 < B ? drr[j + 1] : up_dm;
     link[j] = s + 1 < S && dma == drr[j];
-    nmax = max(nmax, cnt[j]);
   }
-  const int R = __reduce_max_sync(kFull, nmax);
+  const int d0 = __shfl_sync(kFull, drr[0], 0), d1 = __shfl_sync(kFull, drr[B > 1 ? 1 : 0], B > 1 ? 0 : 1);
+  const int R = max(m - L + 1 - d0, S > 1 ? m - d1 : 0);
   if (PROF) {
     int tot = 0;
 #pragma unroll
@@ -1222,12 +1221,8 @@ __device__ long long atlas_row(const Geom& g, int mem_limit, AtlasMem& X, int& e
     for (int m = 0; m < M; ++m) {
       // memory-cap admission (:366-381) + forced drains (:321-346)
       if (PROF) ph_t = clock64();
-      int nblk = 0;
-#pragma unroll
-      for (int j = 0; j < B; ++j)
-        if (lane * B + j < S && m - drr[j] >= mem_limit) ++nblk;
-      nblk = __reduce_add_sync(kFull, nblk);
-      if (nblk > 0) {
+      // some stage blocked <=> stage 0 (the least drained) is
+      if (m - __shfl_sync(kFull, drr[0], 0) >= mem_limit) {
         atlas_cascade<B, TIMELINE, PROF>(g, p, m, mem_limit, X, gfr, drr, wbi, serb, latb, links,
                                          wsuf, n_pairs, n_stage_it, n_rounds, cph);
         if (PROF) ++n_adm;
@@ -1596,8 +1591,7 @@ __device__ void atlas_wave_forward(const Geom& g, int mem_limit, AtlasMem& X, Wa
   }
   __syncwarp();
   for (int m = 0; m < M; ++m) {
-    const int nblk = __reduce_add_sync(kFull, lane < S && m - drr[0] >= mem_limit ? 1 : 0);
-    if (nblk > 0)
+    if (m - __shfl_sync(kFull, drr[0], 0) >= mem_limit)  // stage 0 is the least drained
       atlas_cascade<1, false, false>(g, p, m, mem_limit, X, gfr, drr, wbi, serb, latb, links,
                                      wsuf, n0, n1, n2, nullptr);
     long long gl = lane < S ? gfr[0] - a_loc[0] : -kInf64;
